@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark: harmonic-mean GTEPS of the fused sm_100a BFS over BLEST BVSS structures.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one BFS (init_state + every level, one fused cooperative launch) from the next
+seeded source on the resident BVSS. Default workload (BASELINE.json configs[1]):
+GAP-style Kronecker scale 24 (RMAT a/b/c = .57/.19/.19, edgefactor 16, GAP-style random
+relabel), compression-oriented reorder (auto plan -> Jaccard windows w = 2^16), auto
+engine choice. Graph generation, reordering and BVSS construction run on the GPU before
+the timed region. Inputs (3.4 GB BVSS) exceed the 126 MB L2, so no flush is needed.
+
+N > 1 (torchrun): every rank holds the full structure and runs its own share of the
+sources (no data-path collective, "scaling": "weak"); value = sum over ranks of each
+rank's harmonic-mean GTEPS, each rank timed on its device, the max elapsed over ranks
+reported.
+
+--impl reference: the UNMODIFIED reference engine (oracle/_ref: R:src/bfs_engine.cpp
+run_eager/run_lazy, with workers = all host threads, num_warps = 32 x threads) over the
+same BVSS arrays and sources, on a bounded sample of steps.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kind, params, ordering, description)
+    "c1": ("rmat", dict(scale=16, ef=16, seed=1, relabel=None), "identity",
+           "RMAT scale 16 ef16 (C1), identity order"),
+    "c2": ("rmat", dict(scale=24, ef=16, seed=1, relabel=2), "auto",
+           "GAP-style Kronecker scale 24 ef16, random relabel, compression reorder (auto: Jaccard windows w=2^16)"),
+    "c3": ("urand", dict(scale=24, ef=16, seed=3), "auto",
+           "GAP-style urand scale 24 ef16, ordering as routed by the classifier"),
+    "c4": ("grid", dict(rows=4096, cols=8192, relabel=4), "rcm",
+           "2D 4-neighbour grid 4096x8192 (33.5M vertices), scrambled then RCM"),
+    "c5": ("rmat", dict(scale=27, ef=16, seed=1, relabel=2), "auto",
+           "GAP-style Kronecker scale 27 ef16"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def prepare(config: str, ordering_override: str | None, window: int):
+    """Generate -> (relabel) -> plan/order -> permute -> build, all on the GPU."""
+    import paper_2512_21967_b200 as B
+    kind, prm, ordering, desc = CONFIGS[config]
+    ordering = ordering_override or ordering
+    t0 = time.time()
+    if kind == "rmat":
+        g = B.Graph.generate_rmat(prm["scale"], prm["ef"], prm["seed"])
+    elif kind == "urand":
+        n = 1 << prm["scale"]
+        g = B.Graph.generate_urand(n, prm["ef"] * n, prm["seed"])
+    else:
+        g = B.Graph.generate_grid(prm["rows"], prm["cols"])
+    if prm.get("relabel") is not None:
+        g = B.apply_permutation(g, B.relabel_permutation(g.num_vertices(), prm["relabel"]))
+    t_gen = time.time() - t0
+    t0 = time.time()
+    force = {"auto": None, "identity": B.OrderingStrategy.Identity, "rcm": B.OrderingStrategy.Rcm,
+             "jaccard": B.OrderingStrategy.JaccardWindows, "random": B.OrderingStrategy.Random}[ordering]
+    plan = B.select_plan(g, 8, B.SelectDefaults(window_size=window, force=force))
+    perm = B.make_permutation(g, plan, 8, seed=7)
+    t_order = time.time() - t0
+    t0 = time.time()
+    gp = g if perm.is_identity() else B.apply_permutation(g, perm)
+    b = B.build_bvss(gp)
+    b.producing_permutation = perm
+    b.ordering_tag = plan.strategy.value
+    t_build = time.time() - t0
+    return dict(g=g, gp=gp, b=b, plan=plan, perm=perm, desc=desc, ordering=ordering,
+                times=dict(generate_s=round(t_gen, 3), order_s=round(t_order, 3), build_s=round(t_build, 3)))
+
+
+def b_alg(n, D, P, V, L, lazy):
+    """Algorithmic bytes per BFS: 648 D + 4 P + 4 n + 4 V + k (n/8) L."""
+    return 648 * D + 4 * P + 4 * n + 4 * V + (2 if lazy else 1) * (n // 8) * L
+
+
+def cpu_reference_sample(prep, sources_bvss, mode_lazy, budget_s, threads, max_steps):
+    """Time the reference engine (oracle/_ref) on a bounded sample of the same workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    b = prep["b"]
+    rp, v2r, rows, masks = b.arrays()
+    arr = O.BvssArrays(b.n, b.m, b.num_slice_sets, b.num_vss, b.num_unpadded_slices, rp, v2r, rows, masks)
+    if O.ref_available():
+        rb = O.ref_bvss_from_arrays(arr)
+        kind = "reference"
+        run = lambda s: rb.run(int(s), mode_lazy, warps=32 * threads, workers=threads,
+                               want_levels=False, n=b.n, trace_cap=1 << 16)
+        cores = threads
+    else:
+        kind = "port"
+        run = lambda s: O.run_engine(arr, int(s), mode_lazy)
+        cores = 1
+    times, counters = [], []
+    t_start = time.time()
+    for s in sources_bvss[:max_steps]:
+        t0 = time.perf_counter()
+        r = run(s)
+        times.append(time.perf_counter() - t0)
+        counters.append(r.counters)
+        if time.time() - t_start > budget_s:
+            break
+    del arr
+    return kind, cores, times, counters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "eager", "lazy"])
+    ap.add_argument("--pull", default="popc", choices=["popc", "mma"])
+    ap.add_argument("--order", default=None, choices=["auto", "identity", "rcm", "jaccard", "random"])
+    ap.add_argument("--window", type=int, default=1 << 16)
+    ap.add_argument("--source-seed", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--validate", type=int, default=0, help="check this many sources against the CPU oracle")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference" and rank != 0:
+        return  # the reference arm runs on rank 0 only
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2512_21967_b200 as B
+    from paper_2512_21967_b200 import _lib as L
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+    L.check(lib.blest_set_stream(C.c_void_p(stream.cuda_stream)))
+
+    prep = prepare(args.config, args.order, args.window)
+    g, b, plan, perm = prep["g"], prep["b"], prep["plan"], prep["perm"]
+    cfg = B.EngineConfig(mode=B.engine_mode_from_string(args.mode), pull=args.pull)
+    mode = B.choose_mode(b, plan, cfg)
+    lazy = mode == B.EngineMode.Lazy
+    n = b.n
+    total_sources = args.steps * world + args.warmup
+    srcs_orig = g.pick_sources(total_sources, args.source_seed)
+    srcs = perm.forward_map()[srcs_orig] if not perm.is_identity() else srcs_orig
+    mine = srcs[args.warmup + rank * args.steps: args.warmup + (rank + 1) * args.steps]
+    warm = srcs[: args.warmup]
+    threads = os.cpu_count() or 1
+    workload = dict(workload=args.config, graph=prep["desc"], n=n, arcs=int(b.m),
+                    num_vss=int(b.num_vss), ordering=plan.strategy.value, engine=mode.value,
+                    pull=args.pull, sources=len(mine) * world, source_seed=args.source_seed,
+                    l2="inputs larger than L2 (BVSS %.2f GB > 126 MB), no flush" % (b.num_vss * 644 / 1e9),
+                    prep_s=prep["times"], parallelism=f"source-sharded x{world}" if world > 1 else "1 GPU")
+
+    if args.impl == "reference":
+        t0 = time.time()
+        kind, cores, times, ctrs = cpu_reference_sample(prep, mine, lazy, budget_s=150.0, threads=threads,
+                                                        max_steps=args.steps)
+        # traversed edges per source (bookkeeping for the metric, outside the timed region)
+        ev = [c["E"] for c in census_of(lib, L, b, prep, mine[: len(times)], lazy, args.pull)]
+        hm = len(times) / sum(t / e for t, e in zip(times, ev)) / 1e9
+        line = dict(metric="GTEPS (harmonic mean over sources)", value=round(hm, 6), unit="GTEPS",
+                    n_gpus=1, steps=len(times), warmup=0, ms_per_step=round(1e3 * sum(times) / len(times), 3),
+                    higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
+                    impl="reference", config=workload,
+                    cpu_baseline=dict(value=round(hm, 6), unit="GTEPS", cores=cores, kind=kind,
+                                      sample=f"{len(times)} of {args.steps} sources (bounded ~150 s), "
+                                             f"R:src/bfs_engine.cpp run_{'lazy' if lazy else 'eager'} "
+                                             f"workers={cores} num_warps={32 * cores}"),
+                    e2e=dict(value=round(hm, 6), unit="GTEPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+        print(json.dumps(line), flush=True)
+        return
+
+    ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
+                           L.PULL_MMA if args.pull == "mma" else L.PULL_POPC, 0, 0, 0)
+    ctr = L.CountersT()
+    # ---- census (untimed): deterministic counters + traversed edges per source ----
+    census = census_of(lib, L, b, prep, mine, lazy, args.pull)
+    if args.validate:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        off, tgt = prep["gp"].csr()
+        csr = O.Csr(n, off, tgt)
+        chk = mine[: args.validate]
+        want, _ = O.reference_bfs_many(csr, chk)
+        lv = np.zeros(n, np.uint32)
+        for k, s in enumerate(chk):
+            L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), lv.ctypes.data, C.byref(ctr), None, 0))
+            assert np.array_equal(lv, want[k]), f"levels mismatch for source {int(s)}"
+        log(f"validated {len(chk)} sources bit-exact against the CPU oracle")
+    # ---- warmup ----
+    for s in warm:
+        L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), None, C.byref(ctr), None, 0))
+    # ---- timed region: K fused launches, CUDA events on the launching stream ----
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(mine) + 1)]
+    launches0 = lib.blest_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for k, s in enumerate(mine):
+            L.check(lib.blest_bfs_launch(b.handle, int(s), C.byref(ecfg)))
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.blest_kernel_launches() - launches0
+    L.check(lib.blest_bfs_finish(b.handle, None, C.byref(ctr), None, 0))
+    t = np.array([ev[k].elapsed_time(ev[k + 1]) / 1e3 for k in range(len(mine))])
+    E = np.array([c["E"] for c in census], np.float64)
+    hm = len(t) / float(np.sum(t / E)) / 1e9
+    total_s = float(t.sum())
+    balg = np.array([b_alg(n, c["D"], c["P"], c["V"], c["L"], lazy) for c in census], np.float64)
+    achieved = float(np.sum(balg) / total_s / 1e9)
+    peak, peak_kind = load_peaks()
+    value, elapsed = hm, total_s
+    if world > 1:
+        tt = torch.tensor([hm, total_s], dtype=torch.float64, device="cuda")
+        allv = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(allv, tt)
+        value = float(sum(x[0].item() for x in allv))
+        elapsed = float(max(x[1].item() for x in allv))
+
+    # ---- e2e through the C-ABI with host buffers (pinned) ----
+    e2e = None
+    if not args.no_e2e:
+        hl = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        trace_cap = 1 << 12
+        trace = (L.LevelTraceT * trace_cap)()
+        torch.cuda.synchronize()
+        te = []
+        for s in mine:
+            t0 = time.perf_counter()
+            L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), C.c_void_p(hl.data_ptr()), C.byref(ctr),
+                                  C.cast(trace, C.c_void_p), trace_cap))
+            te.append(time.perf_counter() - t0)
+        te = np.array(te)
+        e2e_hm = len(te) / float(np.sum(te / E)) / 1e9
+        e2e = dict(value=round(e2e_hm * world, 4), unit="GTEPS", h2d_bytes_per_step=4,
+                   d2h_bytes_per_step=int(4 * n + 8 * 8 * min(ctr.trace_len, trace_cap) + 64),
+                   note="blest_bfs(): source in, full level array (pinned host) + counters/trace out, "
+                        "host wall clock per call")
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        kind, cores, ctimes, _ = cpu_reference_sample(prep, mine, lazy, args.cpu_budget, threads, max_steps=8)
+        chm = len(ctimes) / sum(tc / e for tc, e in zip(ctimes, E[: len(ctimes)])) / 1e9
+        cpu = dict(value=round(chm, 6), unit="GTEPS", cores=cores, kind=kind,
+                   sample=f"first {len(ctimes)} of the {len(mine)} timed sources (~{args.cpu_budget:.0f} s budget), "
+                          f"run_{'lazy' if lazy else 'eager'} over the same BVSS arrays")
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        if tj.get("engine") == mode.value and tj.get("pull") == args.pull:
+            traffic = tj.get("dram_bytes_per_launch")
+    if rank == 0:
+        line = dict(
+            metric="GTEPS (harmonic mean over sources)", value=round(value, 4), unit="GTEPS", n_gpus=world,
+            steps=len(mine), warmup=len(warm), ms_per_step=round(1e3 * elapsed / len(mine), 4),
+            higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
+            config=workload,
+            roofline=dict(bound="hbm", achieved=round(achieved, 1), peak=peak, unit="GB/s",
+                          frac=round(achieved / peak, 4), traffic=traffic,
+                          peak_source=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
+                          algorithmic_bytes_per_bfs=int(np.mean(balg)),
+                          formula="648 D + 4 P + 4 n + 4 V + k (n/8) L (SURVEY 8(d))"),
+            cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
+            clocks=clk.summary(),
+            detail=dict(hm_gteps_rank0=round(hm, 4), mean_ms=round(1e3 * float(t.mean()), 4),
+                        min_ms=round(1e3 * float(t.min()), 4), max_ms=round(1e3 * float(t.max()), 4),
+                        mean_dequeues=int(np.mean([c["D"] for c in census])),
+                        mean_levels=float(np.mean([c["L"] for c in census])),
+                        mean_traversed_edges=int(E.mean()), arcs_per_s_G=round(2 * hm, 4)))
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def census_of(lib, L, b, prep, sources, lazy, pull):
+    """Per source: VSS dequeues D, pushes P, visited V, level iterations L and traversed
+    undirected edges E (on the permuted graph, whose ids the level array uses)."""
+    ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
+                           L.PULL_MMA if pull == "mma" else L.PULL_POPC, 0, 0, 0)
+    ctr = L.CountersT()
+    lv_ptr = C.c_void_p()
+    out = []
+    for s in sources:
+        L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), None, C.byref(ctr), None, 0))
+        L.check(lib.blest_bfs_levels_device(b.handle, C.byref(lv_ptr)))
+        e = prep["gp"].traversed_edges(lv_ptr.value)
+        out.append(dict(D=ctr.vss_dequeues, P=ctr.queue_pushes, V=ctr.visited_count, L=ctr.trace_len, E=e))
+    return out
+
+
+if __name__ == "__main__":
+    main()

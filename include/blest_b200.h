@@ -1,0 +1,178 @@
+/*
+ * blest_b200.h — C-ABI of the B200-native BLEST pull-BFS library (libblest_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path (graph load -> reorder ->
+ * BVSS build -> bfs(source) -> level array). The reference is a C++ library with no
+ * FFI (R = /root/reference/proj); each entry point below names the reference
+ * declaration it replaces. The C++ façade include/blest_b200.hpp re-exposes these
+ * with the reference's own names, types and exception classes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. `host` flags say whether array arguments live in
+ *     host memory (1) or device memory (0).
+ *   - Every call returns BLEST_OK (0) or a negative status; blest_last_error() returns the
+ *     message of the calling thread's last failure. Status classes map 1:1 onto the
+ *     reference's exceptions: BLEST_EINVAL = std::invalid_argument, BLEST_ERUNTIME =
+ *     std::runtime_error, BLEST_ELOGIC = std::logic_error.
+ *   - All device work is ordered on one CUDA stream (blest_set_stream; default: the
+ *     legacy default stream). There is no CPU fallback: without a usable sm_100 device
+ *     every compute entry point fails with BLEST_ECUDA.
+ */
+#ifndef BLEST_B200_H
+#define BLEST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLEST_OK 0
+#define BLEST_EINVAL (-1)
+#define BLEST_ERUNTIME (-2)
+#define BLEST_ELOGIC (-3)
+#define BLEST_ECUDA (-4)
+#define BLEST_ENOMEM (-5)
+
+typedef struct blest_graph_s* blest_graph; /* device CSR out-view (blest::Graph, R:include/blest/graph.hpp:38-79) */
+typedef struct blest_bvss_s* blest_bvss;   /* device BVSS + BFS workspace (blest::Bvss, R:include/blest/bvss.hpp:34-63) */
+
+/* EngineMode (R:include/blest/bfs_engine.hpp:14) */
+#define BLEST_MODE_EAGER 0
+#define BLEST_MODE_LAZY 1
+#define BLEST_MODE_AUTO 2
+/* Pull variants: CUDA-core AND+popcount, or the b1 m8n8k128 mma.sync tile (BLEST §4.1). */
+#define BLEST_PULL_POPC 0
+#define BLEST_PULL_MMA 1
+
+/* ---- library ---------------------------------------------------------------------- */
+const char* blest_last_error(void);
+const char* blest_version(void);
+/* Order all subsequent device work on `cuda_stream` (a cudaStream_t; NULL = default). */
+int blest_set_stream(void* cuda_stream);
+/* Device name, SM count, compute capability; fails with BLEST_ECUDA without a device. */
+int blest_device_info(char* name, int name_len, int* sm_count, int* cc_major, int* cc_minor);
+/* Number of library kernels launched so far (process-wide counter; bench evidence). */
+uint64_t blest_kernel_launches(void);
+
+/* ---- graph (R:include/blest/graph.hpp) ----------------------------------------------- */
+/* Graph::from_edges(n, edges, directed) (R:include/blest/graph.hpp:43-44, R:src/graph.cpp:33-55):
+ * mirrors when undirected, range-checks (BLEST_EINVAL), drops self-loops, sorts+dedups. */
+int blest_graph_from_edges(uint32_t n, const uint32_t* src, const uint32_t* dst, uint64_t num_edges,
+                           int directed, int host, blest_graph* out);
+/* CSR out-view (offsets[n+1], targets[m]) -> graph; normalised like from_edges. */
+int blest_graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* targets, int directed,
+                         int host, blest_graph* out);
+/* Harness generators (no reference counterpart): kind 0 = RMAT(scale=a,
+ * edges=k, seed, thresholds t0..t2 as 2^32-scaled probabilities), 1 = urand(n=a, edges=k,
+ * seed), 2 = grid(rows=a, cols=b; R:tests/support/generators.cpp:41-50 semantics). */
+int blest_graph_generate(int kind, uint32_t a, uint32_t b, uint64_t k, uint64_t seed, uint32_t t0,
+                         uint32_t t1, uint32_t t2, blest_graph* out);
+int blest_graph_info(blest_graph g, uint32_t* n, uint64_t* m, int* directed);
+/* Device pointers of the CSR (valid until blest_graph_free). */
+int blest_graph_device_csr(blest_graph g, const uint64_t** offsets, const uint32_t** targets);
+/* out_offsets()/out_targets() copies (R:include/blest/graph.hpp:63-66) into host arrays. */
+int blest_graph_copy_csr(blest_graph g, uint64_t* offsets, uint32_t* targets);
+/* apply_permutation (R:include/blest/graph.hpp:106, R:src/graph.cpp:126-134). forward[old]=new. */
+int blest_graph_apply_permutation(blest_graph g, const uint32_t* forward, int host, blest_graph* out);
+/* Out-degrees (uint32[n]) into host or device memory. */
+int blest_graph_out_degrees(blest_graph g, uint32_t* deg, int host);
+/* Undirected edges in the component reached by a level array: ½·Σ_{L[v]≠∞} outdeg(v)
+ * (the GTEPS numerator); levels in device memory. */
+int blest_graph_traversed_edges(blest_graph g, const uint32_t* levels_dev, uint64_t* edges);
+int blest_graph_free(blest_graph g);
+
+/* ---- ordering (R:include/blest/ordering.hpp) --------------------------------------------- */
+typedef struct {
+    double top1_share, top10_share, power_law_slope, power_law_fit_r2;
+    int is_social_like;
+    int heavy_tail_fired, power_law_fired;
+} blest_social_report;
+/* classify_social_like(g, DegreeSide::Out) (R:include/blest/ordering.hpp:75, R:src/ordering.cpp:346-387) */
+int blest_classify_social_like(blest_graph g, blest_social_report* out);
+/* rcm (R:include/blest/ordering.hpp:56, R:src/ordering.cpp:246-266). forward map into host array. */
+int blest_order_rcm(blest_graph g, uint32_t* forward);
+/* jaccard_with_windows(g, sigma, w, nullptr) (R:include/blest/ordering.hpp:52-53,
+ * R:src/ordering.cpp:139-166) — one CTA per window on the GPU. */
+int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint32_t* forward);
+/* random_order(n, seed) (R:include/blest/ordering.hpp:58, R:src/ordering.cpp:268-275). */
+int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward);
+/* Harness relabel: forward[i] = rank of (splitmix64(seed, i), i); host or device output. */
+int blest_relabel_permutation(uint32_t n, uint64_t seed, uint32_t* forward, int host);
+/* Seeded sources as the CLI samples them (Rng(seed).next_below(n), R:tools/blest.cpp:201-203),
+ * skipping zero-out-degree vertices when skip_isolated != 0. */
+int blest_pick_sources(blest_graph g, uint32_t count, uint64_t seed, int skip_isolated, uint32_t* out);
+
+/* ---- BVSS (R:include/blest/bvss.hpp) ---------------------------------------------------- */
+typedef struct {
+    uint32_t n, num_slice_sets, num_vss, sigma, tau;
+    uint64_t m, num_unpadded_slices;
+} blest_bvss_info;
+typedef struct {
+    double compression_ratio, update_divergence;
+    uint32_t num_slice_sets, num_vss;
+    uint64_t num_slices_padded, num_unpadded_slices, connectivity_bits;
+    uint64_t bytes_real_ptrs, bytes_virtual_to_real, bytes_row_ids, bytes_masks, bytes_dynamic,
+        bytes_levels;
+    uint64_t per_vss_slice_histogram[129]; /* [k] = #VSS with k real slices */
+} blest_bvss_stats_t;
+/* build_bvss(g) (R:include/blest/bvss.hpp:65, R:src/bvss.cpp:19-101) on the GPU. */
+int blest_bvss_build(blest_graph g, blest_bvss* out);
+/* Adopt a host (or device) structure laid out as blest::Bvss's public arrays. */
+int blest_bvss_upload(uint32_t n, uint64_t m, uint32_t num_vss, const uint32_t* real_ptrs,
+                      const uint32_t* virtual_to_real, const uint32_t* row_ids, const uint32_t* masks,
+                      int host, blest_bvss* out);
+int blest_bvss_get_info(blest_bvss b, blest_bvss_info* out);
+/* Copy the four arrays back (host arrays sized per blest_bvss_info). */
+int blest_bvss_download(blest_bvss b, uint32_t* real_ptrs, uint32_t* virtual_to_real, uint32_t* row_ids,
+                        uint32_t* masks);
+/* bvss_stats (R:include/blest/bvss.hpp:97, R:src/bvss.cpp:190-216). */
+int blest_bvss_stats(blest_bvss b, blest_bvss_stats_t* out);
+/* update_divergence alone (R:src/bvss.cpp:109-141), bit-exact with the reference. */
+int blest_bvss_update_divergence(blest_bvss b, double* out);
+int blest_bvss_free(blest_bvss b);
+
+/* ---- BFS (R:include/blest/bfs_engine.hpp) --------------------------------------------- */
+/* EngineConfig (R:include/blest/bfs_engine.hpp:19-25) plus device knobs. */
+typedef struct {
+    int mode;              /* BLEST_MODE_EAGER / BLEST_MODE_LAZY (AUTO is resolved by the caller) */
+    int pull;              /* BLEST_PULL_POPC / BLEST_PULL_MMA */
+    uint32_t max_levels;   /* 0 = n + 1 */
+    uint32_t num_warps;    /* logical warps for the round-robin VSS split; 0 = whole grid */
+    uint32_t grid_ctas;    /* 0 = persistent grid (all co-resident CTAs) */
+} blest_engine_config;
+/* EngineCounters (R:include/blest/bfs_engine.hpp:39-50) + BfsResult scalars (graph.hpp:111-116). */
+typedef struct {
+    uint64_t mma_calls, full_atomics, relaxed_atomics, queue_pushes, vss_dequeues,
+        brs_baseline_mma_calls;
+    uint32_t levels_processed;
+    uint32_t num_levels;
+    uint64_t visited_count;
+    uint32_t trace_len;       /* level iterations (including the barren last one) */
+    uint32_t trace_truncated; /* trace rows beyond the device capacity were folded */
+} blest_counters;
+/* LevelTrace (R:include/blest/bfs_engine.hpp:27-37), per_warp_mma omitted. */
+typedef struct {
+    uint64_t level, queue_size, frontier_population, discovered, full_atomics, stage1_full_atomics,
+        relaxed_atomics, queue_pushes;
+} blest_level_trace;
+
+/* run_eager / run_lazy (R:include/blest/bfs_engine.hpp:70-78, R:src/bfs_engine.cpp:155-350):
+ * synchronous. levels_out (host, n entries) may be NULL; trace_out may be NULL. Throws-
+ * equivalents: BLEST_EINVAL (src >= n), BLEST_ERUNTIME (level cap exceeded). */
+int blest_bfs(blest_bvss b, uint32_t src, const blest_engine_config* cfg, uint32_t* levels_out,
+              blest_counters* counters, blest_level_trace* trace_out, uint32_t trace_cap);
+/* Asynchronous split of blest_bfs for stream-ordered timing: launch enqueues the fused
+ * kernel (init + all levels) on the library stream; finish waits and reads back. */
+int blest_bfs_launch(blest_bvss b, uint32_t src, const blest_engine_config* cfg);
+int blest_bfs_finish(blest_bvss b, uint32_t* levels_out, blest_counters* counters,
+                     blest_level_trace* trace_out, uint32_t trace_cap);
+/* Device pointer to the level array of the last run on b (n entries). */
+int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
+/* Launch geometry of the last run (CTAs, threads per CTA). */
+int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLEST_B200_H */

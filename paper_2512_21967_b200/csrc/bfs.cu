@@ -1,0 +1,496 @@
+// Fused persistent BFS kernel for sm_100a: one cooperative launch per source runs
+// init_state and every level, with a grid barrier replacing the reference's per-level
+// fork/join (R:src/bfs_engine.cpp:187, :273, :299).
+//
+// Work unit = one VSS (R:include/blest/bvss.hpp:34-63) handled by one warp: lane t reads
+// its mask word (one coalesced 128 B line per VSS) and its 4 row ids (one 16 B load; four
+// 128 B lines per VSS), both with streaming (evict-first, no-L1) loads. Warps take queue
+// positions round-robin exactly like the reference (p ≡ warp mod #warps, :190), B
+// positions at a time so each lane keeps 2·B independent HBM loads in flight.
+//
+// Queue entries are 64-bit: low = VSS id, high = aux. Eager: aux = slice set (saves the
+// virtual_to_real lookup, :192). Lazy: aux = the slice set's frontier byte α, final when
+// stage 2 enqueues (saves the F_curr read, :281-282).
+//
+// Eager (Alg. 2, :155-236): one grid barrier per level. Frontier bitmaps F are
+// triple-buffered: level ℓ reads F[ℓ%3] (α), atomically ORs discoveries into F[(ℓ+1)%3],
+// and zeroes the bytes of F[(ℓ+2)%3] that level ℓ-1 used (found from queue ℓ-1), so no
+// Θ(n) clear is ever needed (the reference clears all words per level, :227-228).
+// Lazy (Alg. 3, :238-350): stage 1 pulls with fire-and-forget REDs into V_next (skipped
+// when V_curr already has the bit — legal per SURVEY §8(a) pitfall 7); barrier; stage 2
+// sweeps ⌈n/32⌉ words, writes levels with coalesced 128 B stores and enqueues; barrier.
+//
+// Enqueue (both modes): lanes append slice sets to a per-warp shared-memory buffer; a
+// flush reserves queue space with ONE atomicAdd per warp-buffer (warp-aggregated
+// reservation, PAPER §4.2) and expands each set's VSS range [real_ptrs[s], real_ptrs[s+1]).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "bfs.cuh"
+
+namespace blestgpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr int kBatch = 4;         // VSSs in flight per warp
+constexpr int kPushCap = 64;      // per-warp push buffer entries
+constexpr unsigned long long kNoEntry = ~0ull;
+
+struct Params {
+    uint32_t n, num_sets;
+    uint64_t words;
+    const uint32_t* __restrict__ rp;
+    const uint32_t* __restrict__ masks;
+    const uint4* __restrict__ rows4;
+    uint32_t* L;
+    uint32_t* B0;  // eager F0 / lazy V_curr
+    uint32_t* B1;  // eager F1 / lazy V_next
+    uint32_t* B2;  // eager F2
+    unsigned long long* Q0;
+    unsigned long long* Q1;
+    unsigned long long* Q2;
+    unsigned long long* ctl;    // [0..3] qlen ring, [4] iterations, [5] max level, [6] status
+    unsigned* bar;
+    unsigned long long* trace;
+    uint32_t trace_cap;
+    uint32_t src;
+    uint32_t cap;
+    uint32_t num_warps;
+};
+
+struct Smem {
+    unsigned long long push[kWarpsPerCta][kPushCap];  // ss | aux << 32
+    unsigned long long ctr[4];                        // discovered, full, relaxed, pushes
+};
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+// Fire-and-forget OR (REDG): the lazy scheme's "relaxed atomic" (R:src/bfs_engine.cpp:287-288).
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int MODE>
+__device__ __forceinline__ unsigned long long* queue_at(const Params& p, uint32_t idx) {
+    if (MODE == 0) {
+        const uint32_t k = idx % 3;
+        return k == 0 ? p.Q0 : (k == 1 ? p.Q1 : p.Q2);
+    }
+    return (idx & 1) ? p.Q1 : p.Q0;
+}
+
+__device__ __forceinline__ uint32_t* fbuf(const Params& p, uint32_t idx) {
+    const uint32_t k = idx % 3;
+    return k == 0 ? p.B0 : (k == 1 ? p.B1 : p.B2);
+}
+
+// Warp flush: reserve room for the buffered slice sets' VSS ranges with one atomicAdd and
+// write the expanded entries. Returns VSS entries written (for the trace).
+__device__ uint32_t flush_pushes(const Params& p, unsigned long long* buf, uint32_t& count,
+                                 unsigned long long* Qn, unsigned long long* qlen_next) {
+    const unsigned lane = lane_id();
+    uint32_t total = 0;
+    uint32_t my_off[kPushCap / 32], my_b[kPushCap / 32], my_len[kPushCap / 32];
+#pragma unroll
+    for (int k = 0; k < kPushCap / 32; ++k) {
+        const uint32_t i = k * 32 + lane;
+        uint32_t b = 0, len = 0;
+        if (i < count) {
+            const uint32_t ss = (uint32_t)buf[i];
+            b = p.rp[ss];
+            len = p.rp[ss + 1] - b;
+        }
+        const uint32_t incl = warp_incl_scan(len);
+        my_off[k] = total + incl - len;
+        my_b[k] = b;
+        my_len[k] = len;
+        total += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    unsigned long long base = 0;
+    if (lane == 0 && total) base = atomicAdd(qlen_next, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t i = 0; i < count; ++i) {
+        const int k = i >> 5;
+        const uint32_t src_lane = i & 31;
+        uint32_t off = 0, b = 0, len = 0;
+#pragma unroll
+        for (int kk = 0; kk < kPushCap / 32; ++kk)
+            if (kk == k) {
+                off = __shfl_sync(0xffffffffu, my_off[kk], src_lane);
+                b = __shfl_sync(0xffffffffu, my_b[kk], src_lane);
+                len = __shfl_sync(0xffffffffu, my_len[kk], src_lane);
+            }
+        const unsigned long long aux = buf[i] & 0xFFFFFFFF00000000ull;
+        for (uint32_t t = lane; t < len; t += 32) Qn[base + off + t] = aux | (unsigned long long)(b + t);
+    }
+    __syncwarp();
+    count = 0;
+    return total;
+}
+
+// Append per-lane push flags for one column to the warp buffer (flushing first if full).
+__device__ __forceinline__ void push_column(const Params& p, bool flag, unsigned long long item,
+                                            unsigned long long* buf, uint32_t& count,
+                                            unsigned long long* Qn, unsigned long long* qlen_next,
+                                            uint32_t& pushes, uint32_t& full) {
+    const unsigned ball = __ballot_sync(0xffffffffu, flag);
+    if (!ball) return;
+    const uint32_t k = __popc(ball);
+    if (count + k > kPushCap) {
+        pushes += flush_pushes(p, buf, count, Qn, qlen_next);
+        full += 1;
+    }
+    if (flag) buf[count + __popc(ball & ((1u << lane_id()) - 1))] = item;
+    __syncwarp();
+    count += k;
+}
+
+template <int PULL>
+__device__ __forceinline__ void column_counts(uint32_t m, uint32_t alpha, uint32_t (&cnt)[4]) {
+    if (PULL == 0) {
+        // CUDA-core path: AND with the broadcast frontier byte, per-byte nonzero test.
+        const uint32_t x = m & (alpha * 0x01010101u);
+        cnt[0] = x & 0xFFu;
+        cnt[1] = (x >> 8) & 0xFFu;
+        cnt[2] = (x >> 16) & 0xFFu;
+        cnt[3] = x >> 24;
+    } else {
+        // BLEST tile: 2 × m8n8k128 b1 AND+POPC per VSS. fragB: lanes 9r hold α, lanes 9r+4
+        // hold α<<8 (build_fragB, R:src/tc_emu.cpp:22-29); fragA = the lane's low/high 16
+        // mask bits per round (pack_fragA_round :31-38); lane t gets its own two column
+        // popcounts (lane_dot_products :40-45).
+        const unsigned lane = lane_id();
+        const uint32_t r9 = lane % 9;
+        const uint32_t b = (r9 == 0) ? alpha : ((r9 == 4) ? (alpha << 8) : 0u);
+#pragma unroll
+        for (int round = 0; round < 2; ++round) {
+            const uint32_t a = round ? (m >> 16) : (m & 0xFFFFu);
+            int d0 = 0, d1 = 0;
+            asm volatile(
+                "mma.sync.aligned.m8n8k128.row.col.s32.b1.b1.s32.and.popc "
+                "{%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+r"(d0), "+r"(d1)
+                : "r"(a), "r"(b));
+            cnt[2 * round] = (uint32_t)d0;
+            cnt[2 * round + 1] = (uint32_t)d1;
+        }
+    }
+}
+
+// Flush per-thread counters into the CTA's shared counters, then (thread 0) into the
+// level's trace row; then the grid barrier.
+__device__ __forceinline__ void level_barrier(const Params& p, Smem& sm, unsigned& gen, uint32_t level,
+                                              uint32_t (&c)[4], bool count_level) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t s = warp_sum(c[i]);
+        if (lane_id() == 0 && s) atomicAdd(&sm.ctr[i], (unsigned long long)s);
+        c[i] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && count_level) {
+        const uint32_t row = min(level - 1, p.trace_cap - 1);
+        unsigned long long* t = p.trace + 8ull * row;
+        if (sm.ctr[0]) {
+            atomicAdd(&t[3], sm.ctr[0]);
+            atomicMax(&p.ctl[5], (unsigned long long)level);
+        }
+        if (sm.ctr[1]) atomicAdd(&t[4], sm.ctr[1]);
+        if (sm.ctr[2]) atomicAdd(&t[6], sm.ctr[2]);
+        if (sm.ctr[3]) atomicAdd(&t[7], sm.ctr[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sm.ctr[i] = 0;
+    }
+    grid_barrier(p.bar, gen);
+}
+
+template <int MODE, int PULL>
+__global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
+    __shared__ Smem sm;
+    const unsigned lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint64_t gtid = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
+    const uint64_t gthreads = (uint64_t)gridDim.x * kThreads;
+    const uint32_t gw = blockIdx.x * kWarpsPerCta + warp;
+    const uint32_t all_warps = gridDim.x * kWarpsPerCta;
+    const uint32_t NW = (p.num_warps && p.num_warps < all_warps) ? p.num_warps : all_warps;
+    unsigned gen = 0;
+    const uint64_t pol = evict_first_policy();
+    if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
+
+    // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
+    const uint32_t src = p.src;
+    const uint32_t sset = src / kSigma;
+    const uint32_t seed_b = p.rp[sset], seed_e = p.rp[sset + 1];
+    for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
+    const uint32_t src_word = src >> 5, src_bit = 1u << (src & 31);
+    for (uint64_t w = gtid; w < p.words; w += gthreads) {
+        const uint32_t seed = (w == src_word) ? src_bit : 0u;
+        if (MODE == 0) {
+            p.B0[w] = 0;
+            p.B1[w] = seed;  // F[1] = F_curr of level 1
+            p.B2[w] = 0;
+        } else {
+            p.B0[w] = seed;  // V_curr
+            p.B1[w] = seed;  // V_next
+        }
+    }
+    {
+        unsigned long long* Q1 = p.Q1;
+        const unsigned long long aux =
+            (MODE == 0) ? ((unsigned long long)sset << 32)
+                        : ((unsigned long long)(1u << (src & 7)) << 32);
+        for (uint64_t i = gtid; i < seed_e - seed_b; i += gthreads) Q1[i] = aux | (seed_b + i);
+    }
+    if (gtid == 0) {
+        p.ctl[0] = 0;
+        p.ctl[1] = seed_e - seed_b;
+        p.ctl[2] = 0;
+        p.ctl[3] = 0;
+        p.ctl[4] = 0;
+        p.ctl[5] = 0;
+        p.ctl[6] = 0;
+        for (int i = 0; i < 8; ++i) p.trace[i] = 0;
+    }
+    grid_barrier(p.bar, gen);
+
+    unsigned long long* pbuf = sm.push[warp];
+    uint32_t pcount = 0;
+    uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
+    uint32_t level = 1;
+    for (;; ++level) {
+        const unsigned long long len = ld_relaxed_gpu_u64(&p.ctl[level & 3]);
+        if (len == 0) break;
+        if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
+            if (gtid == 0) p.ctl[6] = 1;
+            break;
+        }
+        if (gtid == 0) {
+            p.ctl[(level + 2) & 3] = 0;
+            if (level - 1 < p.trace_cap) {
+                p.trace[8ull * (level - 1) + 0] = level;
+                p.trace[8ull * (level - 1) + 1] = len;
+            } else {
+                atomicAdd(&p.trace[8ull * (p.trace_cap - 1) + 1], len);
+            }
+            if (level < p.trace_cap)
+                for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
+        }
+        unsigned long long* Qc = queue_at<MODE>(p, level);
+        unsigned long long* Qn = queue_at<MODE>(p, level + 1);
+        unsigned long long* qlen_next = &p.ctl[(level + 1) & 3];
+        const uint32_t* Fc = (MODE == 0) ? fbuf(p, level) : nullptr;
+        uint32_t* Fn = (MODE == 0) ? fbuf(p, level + 1) : p.B1;
+        const uint32_t* Vc = p.B0;
+
+        if (MODE == 0) {
+            // Zero the frontier bytes level ℓ-1 read: they become F_next at ℓ+1.
+            uint8_t* Fz = reinterpret_cast<uint8_t*>(fbuf(p, level + 2));
+            const unsigned long long* Qz = queue_at<MODE>(p, level + 2);
+            const unsigned long long zlen = ld_relaxed_gpu_u64(&p.ctl[(level + 3) & 3]);
+            for (uint64_t i = gtid; i < zlen; i += gthreads) Fz[Qz[i] >> 32] = 0;
+        }
+
+        // ---- pull over the queue (pull_vss, R:src/bfs_engine.cpp:131-146) ----
+        if (gw < NW) {
+            for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
+                unsigned long long e = kNoEntry;
+                if (lane < kBatch) {
+                    const uint64_t pos = p0 + (uint64_t)lane * NW;
+                    if (pos < len) e = Qc[pos];
+                }
+                uint32_t alpha_l = 0;
+                if (MODE == 0 && e != kNoEntry) {
+                    const uint32_t ss = (uint32_t)(e >> 32);
+                    alpha_l = reinterpret_cast<const uint8_t*>(Fc)[ss];  // frontier_byte :148-151
+                }
+                uint32_t mk[kBatch];
+                uint4 rw[kBatch];
+                unsigned long long ej[kBatch];
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    ej[j] = __shfl_sync(0xffffffffu, e, j);
+                    mk[j] = 0;
+                    rw[j] = make_uint4(0, 0, 0, 0);
+                    if (ej[j] != kNoEntry) {
+                        const uint64_t v = (uint32_t)ej[j];
+                        mk[j] = ld_stream_u32(p.masks + 32 * v + lane, pol);
+                        rw[j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    if (ej[j] == kNoEntry) continue;  // warp-uniform
+                    const uint32_t alpha = (MODE == 0) ? __shfl_sync(0xffffffffu, alpha_l, j)
+                                                       : (uint32_t)((ej[j] >> 32) & 0xFFu);
+                    uint32_t cnt[4];
+                    column_counts<PULL>(mk[j], alpha, cnt);
+                    const uint32_t rr[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        bool push = false;
+                        uint32_t u = rr[c];
+                        if (cnt[c]) {
+                            const uint32_t bit = 1u << (u & 31);
+                            if (MODE == 1) {
+                                // stage-1 sink (:286-289): relaxed OR into V_next
+                                if (!(Vc[u >> 5] & bit)) {
+                                    red_or(Fn + (u >> 5), bit);
+                                    ++ctr[2];
+                                }
+                            } else if (p.L[u] == kInf) {  // eager sink (:198-211)
+                                const uint32_t old = atomicOr(Fn + (u >> 5), bit);
+                                ++ctr[1];
+                                if (!(old & bit)) {
+                                    p.L[u] = level;
+                                    ++ctr[0];
+                                    push = ((old >> (8 * ((u >> 3) & 3))) & 0xFFu) == 0;
+                                }
+                            }
+                        }
+                        if (MODE == 0)
+                            push_column(p, push, (unsigned long long)(u >> 3) << 32 | (u >> 3), pbuf,
+                                        pcount, Qn, qlen_next, ctr[3], ctr[1]);
+                    }
+                }
+            }
+        }
+
+        if (MODE == 1) {
+            level_barrier(p, sm, gen, level, ctr, true);
+            // ---- stage 2 (R:src/bfs_engine.cpp:296-338): word sweep ----
+            uint32_t* Vn = p.B1;
+            uint32_t* Vcw = p.B0;
+            for (uint64_t wb = (uint64_t)gw * 32; wb < p.words; wb += (uint64_t)all_warps * 32) {
+                const uint64_t w = wb + lane;
+                uint32_t diff = 0, nx = 0;
+                if (w < p.words) {
+                    nx = Vn[w];
+                    diff = nx & ~Vcw[w];
+                    if (diff) Vcw[w] = nx;
+                }
+                ctr[0] += __popc(diff);
+                unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
+                while (ball) {
+                    const int k = __ffs(ball) - 1;
+                    ball &= ball - 1;
+                    const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
+                    if ((dk >> lane) & 1u) p.L[32 * (wb + k) + lane] = level;
+                }
+#pragma unroll
+                for (int bsel = 0; bsel < 4; ++bsel) {
+                    const uint32_t alpha = (diff >> (8 * bsel)) & 0xFFu;
+                    const uint64_t ss = 4 * w + bsel;
+                    push_column(p, alpha != 0, (unsigned long long)alpha << 32 | ss, pbuf, pcount, Qn,
+                                qlen_next, ctr[3], ctr[1]);
+                }
+            }
+        }
+        if (pcount) {
+            ctr[3] += flush_pushes(p, pbuf, pcount, Qn, qlen_next);
+            ctr[1] += 1;
+        }
+        level_barrier(p, sm, gen, level, ctr, true);
+    }
+    if (gtid == 0) p.ctl[4] = level - 1;
+}
+
+}  // namespace
+
+BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
+    words_ = ((uint64_t)b.n + 31) / 32;
+    const uint64_t levels_bound = (uint64_t)b.n + 2;
+    trace_cap_ = (uint32_t)std::min<uint64_t>(levels_bound, 1u << 20);
+    levels_.alloc(b.n ? b.n : 1);
+    bits_.alloc(3 * (words_ ? words_ : 1));
+    q_.alloc(3 * (uint64_t)(b.num_vss ? b.num_vss : 1));
+    ctl_.alloc(8);
+    bar_.alloc(2);
+    trace_.alloc(8ull * trace_cap_);
+    CK(cudaMallocHost(&pinned_, 8 * sizeof(unsigned long long)));
+}
+
+BfsEngine::~BfsEngine() {
+    if (pinned_) cudaFreeHost(pinned_);
+}
+
+void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
+    if (src >= b_.n) throw InvalidArgument("bfs source out of range");
+    const int mode = (int)opt.mode, pull = (int)opt.pull;
+    void (*kern)(Params) = nullptr;
+    if (mode == 0 && pull == 0) kern = k_bfs<0, 0>;
+    else if (mode == 0 && pull == 1) kern = k_bfs<0, 1>;
+    else if (mode == 1 && pull == 0) kern = k_bfs<1, 0>;
+    else kern = k_bfs<1, 1>;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+    if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
+    uint32_t ctas = (uint32_t)per_sm * (uint32_t)num_sms();
+    if (opt.grid_ctas && opt.grid_ctas < ctas) ctas = opt.grid_ctas;
+    Params p{};
+    p.n = b_.n;
+    p.num_sets = b_.num_sets;
+    p.words = words_;
+    p.rp = b_.real_ptrs.p;
+    p.masks = b_.masks.p;
+    p.rows4 = reinterpret_cast<const uint4*>(b_.row_ids.p);
+    p.L = levels_.p;
+    p.B0 = bits_.p;
+    p.B1 = bits_.p + words_;
+    p.B2 = bits_.p + 2 * words_;
+    const uint64_t qcap = b_.num_vss ? b_.num_vss : 1;
+    p.Q0 = q_.p;
+    p.Q1 = q_.p + qcap;
+    p.Q2 = q_.p + 2 * qcap;
+    p.ctl = ctl_.p;
+    p.bar = bar_.p;
+    p.trace = trace_.p;
+    p.trace_cap = trace_cap_;
+    p.src = src;
+    p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
+    p.num_warps = opt.num_warps;
+    cudaStream_t st = stream();
+    CK(cudaMemsetAsync(bar_.p, 0, 2 * sizeof(unsigned), st));
+    void* args[] = {&p};
+    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(ctas), dim3(kThreads), args, 0, st));
+    last_ctas_ = ctas;
+    last_threads_ = kThreads;
+    last_src_ = src;
+    last_mode_ = opt.mode;
+    launched_ = true;
+}
+
+BfsOutcome BfsEngine::finish(uint32_t* levels_host) {
+    if (!launched_) throw LogicError("finish() without launch()");
+    cudaStream_t st = stream();
+    CK(cudaMemcpyAsync(pinned_, ctl_.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (levels_host && b_.n)
+        CK(cudaMemcpyAsync(levels_host, levels_.p, (size_t)b_.n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    BfsOutcome out;
+    out.iterations = (uint32_t)pinned_[4];
+    out.max_level = (uint32_t)pinned_[5];
+    const bool runaway = pinned_[6] != 0;
+    const uint32_t rows = std::min(out.iterations, trace_cap_);
+    out.trace_truncated = out.iterations > trace_cap_;
+    out.trace.resize(rows);
+    if (rows)
+        CK(cudaMemcpy(out.trace.data(), trace_.p, rows * sizeof(TraceRow), cudaMemcpyDeviceToHost));
+    uint64_t visited = 1;
+    for (uint32_t i = 0; i < rows; ++i) {
+        TraceRow& r = out.trace[i];
+        visited += r.discovered;
+        r.frontier_population = (i == 0) ? 1 : out.trace[i - 1].discovered;
+        r.stage1_full_atomics = (last_mode_ == Mode::Eager) ? r.full_atomics : 0;
+    }
+    out.visited = visited;
+    if (runaway)
+        throw RuntimeError("BFS ran past the level safety cap at level " +
+                           std::to_string(out.iterations + 1) + " — engine invariant broken");
+    return out;
+}
+
+}  // namespace blestgpu

@@ -1,0 +1,73 @@
+// The fused persistent BFS engine (eager = Alg. 2, lazy = Alg. 3) over a DeviceBvss.
+// Reference: run_eager / run_lazy (R:src/bfs_engine.cpp:155-350), pull_vss (:131-146),
+// init_state (:30-49), counters (R:include/blest/bfs_engine.hpp:27-50).
+#pragma once
+
+#include <vector>
+
+#include "bvss.cuh"
+
+namespace blestgpu {
+
+enum class Mode : int { Eager = 0, Lazy = 1 };
+enum class Pull : int { Popc = 0, Mma = 1 };  // CUDA-core popcount vs b1 mma.sync tile
+
+struct EngineOptions {
+    Mode mode = Mode::Eager;
+    Pull pull = Pull::Popc;
+    uint32_t max_levels = 0;  // 0 = n + 1 (R:src/bfs_engine.cpp:68-70)
+    uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
+    uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
+};
+
+// One row per level, same fields as LevelTrace (R:include/blest/bfs_engine.hpp:27-37).
+struct TraceRow {
+    uint64_t level, queue_size, frontier_population, discovered, full_atomics,
+        stage1_full_atomics, relaxed_atomics, queue_pushes;
+};
+
+struct BfsOutcome {
+    uint32_t iterations = 0;  // trace length (includes the barren final level)
+    uint32_t max_level = 0;   // levels_processed
+    uint64_t visited = 0;
+    bool trace_truncated = false;
+    std::vector<TraceRow> trace;
+};
+
+// Per-structure device workspace; sized once, reused across sources.
+class BfsEngine {
+public:
+    explicit BfsEngine(const DeviceBvss& b);
+    ~BfsEngine();
+    BfsEngine(const BfsEngine&) = delete;
+    BfsEngine& operator=(const BfsEngine&) = delete;
+
+    // Enqueue init + the fused level loop on stream() (no host sync). Throws on bad args.
+    void launch(uint32_t src, const EngineOptions& opt);
+    // Wait for the last launch, read back trace/counters, check status (throws
+    // RuntimeError past the level cap). Copies levels to host when levels_host != null.
+    BfsOutcome finish(uint32_t* levels_host);
+    const uint32_t* levels_device() const { return levels_.p; }
+    uint32_t trace_capacity() const { return trace_cap_; }
+    uint32_t last_grid_ctas() const { return last_ctas_; }
+    uint32_t last_threads() const { return last_threads_; }
+    uint32_t last_src() const { return last_src_; }
+    const DeviceBvss& bvss() const { return b_; }
+
+private:
+    const DeviceBvss& b_;
+    uint64_t words_ = 0;
+    uint32_t trace_cap_ = 0;
+    DevBuf<uint32_t> levels_;
+    DevBuf<uint32_t> bits_;              // 3 * words_
+    DevBuf<unsigned long long> q_;       // 3 * max(num_vss, 1) entries
+    DevBuf<unsigned long long> ctl_;     // qlen[4], result[4]
+    DevBuf<unsigned> bar_;               // grid barrier [2]
+    DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
+    unsigned long long* pinned_ = nullptr;  // host mirror for ctl_ readback
+    uint32_t last_ctas_ = 0, last_threads_ = 0, last_src_ = 0;
+    Mode last_mode_ = Mode::Eager;
+    bool launched_ = false;
+};
+
+}  // namespace blestgpu

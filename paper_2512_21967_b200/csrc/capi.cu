@@ -1,0 +1,486 @@
+// extern "C" boundary (include/blest_b200.h). Every entry point catches C++ exceptions
+// and maps them onto status codes with the reference's exception classes.
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/blest_b200.h"
+#include "bfs.cuh"
+#include "bvss.cuh"
+#include "graph.cuh"
+#include "ordering.cuh"
+
+using namespace blestgpu;
+
+struct blest_graph_s {
+    DeviceGraph g;
+};
+struct blest_bvss_s {
+    DeviceBvss b;
+    std::unique_ptr<BfsEngine> engine;
+    BfsEngine& eng() {
+        if (!engine) engine = std::make_unique<BfsEngine>(b);
+        return *engine;
+    }
+};
+
+namespace blestgpu {
+namespace {
+cudaStream_t g_stream = nullptr;
+int g_sms = 0;
+}  // namespace
+cudaStream_t stream() { return g_stream; }
+void set_stream(cudaStream_t s) { g_stream = s; }
+int num_sms() {
+    if (!g_sms) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return g_sms;
+}
+std::atomic<uint64_t> g_launches{0};
+}  // namespace blestgpu
+
+namespace {
+thread_local std::string t_err;
+
+int fail_with(int code, const char* what) {
+    t_err = what;
+    return code;
+}
+
+void require_device() {
+    static int ok = -1;
+    if (ok < 0) {
+        int count = 0;
+        const cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            ok = 0;
+        } else {
+            int dev = 0, major = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+            ok = major >= 10 ? 1 : 0;
+        }
+    }
+    if (!ok) throw CudaError("no sm_100 CUDA device available (libblest_b200 has no CPU fallback)");
+}
+}  // namespace
+
+#define API_BEGIN try {
+#define API_END                                                              \
+    return BLEST_OK;                                                         \
+    }                                                                        \
+    catch (const InvalidArgument& e) { return fail_with(BLEST_EINVAL, e.what()); } \
+    catch (const RuntimeError& e) { return fail_with(BLEST_ERUNTIME, e.what()); }  \
+    catch (const LogicError& e) { return fail_with(BLEST_ELOGIC, e.what()); }      \
+    catch (const CudaError& e) { return fail_with(BLEST_ECUDA, e.what()); }        \
+    catch (const std::bad_alloc& e) { return fail_with(BLEST_ENOMEM, e.what()); }  \
+    catch (const std::invalid_argument& e) { return fail_with(BLEST_EINVAL, e.what()); } \
+    catch (const std::exception& e) { return fail_with(BLEST_ERUNTIME, e.what()); }
+
+#define NEED(p, msg) \
+    if (!(p)) throw InvalidArgument(msg)
+
+extern "C" {
+
+const char* blest_last_error(void) { return t_err.c_str(); }
+const char* blest_version(void) { return "blest_b200 0.1 (sm_100a)"; }
+uint64_t blest_kernel_launches(void) { return g_launches.load(); }
+
+int blest_set_stream(void* s) {
+    API_BEGIN
+    set_stream(reinterpret_cast<cudaStream_t>(s));
+    API_END
+}
+
+int blest_device_info(char* name, int name_len, int* sm_count, int* cc_major, int* cc_minor) {
+    API_BEGIN
+    require_device();
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (name && name_len > 0) {
+        std::strncpy(name, prop.name, name_len - 1);
+        name[name_len - 1] = 0;
+    }
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (cc_major) *cc_major = prop.major;
+    if (cc_minor) *cc_minor = prop.minor;
+    API_END
+}
+
+// ---- graph ------------------------------------------------------------------------------
+int blest_graph_from_edges(uint32_t n, const uint32_t* src, const uint32_t* dst, uint64_t k,
+                           int directed, int host, blest_graph* out) {
+    API_BEGIN
+    NEED(out, "out is null");
+    NEED(k == 0 || (src && dst), "edge arrays are null");
+    require_device();
+    auto h = std::make_unique<blest_graph_s>();
+    h->g = graph_from_edges(n, src, dst, k, directed != 0, host != 0);
+    *out = h.release();
+    API_END
+}
+
+int blest_graph_from_csr(uint32_t n, const uint64_t* off, const uint32_t* tgt, int directed, int host,
+                         blest_graph* out) {
+    API_BEGIN
+    NEED(out && off, "null argument");
+    require_device();
+    auto h = std::make_unique<blest_graph_s>();
+    h->g = graph_from_csr(n, off, tgt, directed != 0, host != 0);
+    *out = h.release();
+    API_END
+}
+
+int blest_graph_generate(int kind, uint32_t a, uint32_t b, uint64_t k, uint64_t seed, uint32_t t0,
+                         uint32_t t1, uint32_t t2, blest_graph* out) {
+    API_BEGIN
+    NEED(out, "out is null");
+    require_device();
+    auto h = std::make_unique<blest_graph_s>();
+    switch (kind) {
+        case 0: h->g = graph_generate_rmat(a, k, seed, t0, t1, t2); break;
+        case 1: h->g = graph_generate_urand(a, k, seed); break;
+        case 2: h->g = graph_generate_grid(a, b); break;
+        default: throw InvalidArgument("unknown generator kind");
+    }
+    *out = h.release();
+    API_END
+}
+
+int blest_graph_info(blest_graph g, uint32_t* n, uint64_t* m, int* directed) {
+    API_BEGIN
+    NEED(g, "null graph");
+    if (n) *n = g->g.n;
+    if (m) *m = g->g.m;
+    if (directed) *directed = g->g.directed ? 1 : 0;
+    API_END
+}
+
+int blest_graph_device_csr(blest_graph g, const uint64_t** off, const uint32_t** tgt) {
+    API_BEGIN
+    NEED(g, "null graph");
+    if (off) *off = g->g.off.p;
+    if (tgt) *tgt = g->g.tgt.p;
+    API_END
+}
+
+int blest_graph_copy_csr(blest_graph g, uint64_t* off, uint32_t* tgt) {
+    API_BEGIN
+    NEED(g, "null graph");
+    if (off) CK(cudaMemcpyAsync(off, g->g.off.p, ((size_t)g->g.n + 1) * 8, cudaMemcpyDeviceToHost, stream()));
+    if (tgt && g->g.m) CK(cudaMemcpyAsync(tgt, g->g.tgt.p, g->g.m * 4, cudaMemcpyDeviceToHost, stream()));
+    CK(cudaStreamSynchronize(stream()));
+    API_END
+}
+
+int blest_graph_apply_permutation(blest_graph g, const uint32_t* forward, int host, blest_graph* out) {
+    API_BEGIN
+    NEED(g && forward && out, "null argument");
+    const uint32_t n = g->g.n;
+    DevBuf<uint32_t> f(n ? n : 1);
+    std::vector<uint32_t> hf(n);
+    if (host) std::memcpy(hf.data(), forward, (size_t)n * 4);
+    else CK(cudaMemcpy(hf.data(), forward, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    // Permutation::from_forward bijection check (R:src/graph.cpp:86-99)
+    std::vector<char> seen(n, 0);
+    for (uint32_t i = 0; i < n; ++i) {
+        if (hf[i] >= n || seen[hf[i]]) throw InvalidArgument("permutation is not a bijection on [0, n)");
+        seen[hf[i]] = 1;
+    }
+    if (n) CK(cudaMemcpyAsync(f.p, hf.data(), (size_t)n * 4, cudaMemcpyHostToDevice, stream()));
+    auto h = std::make_unique<blest_graph_s>();
+    h->g = graph_permute(g->g, f.p);
+    *out = h.release();
+    API_END
+}
+
+int blest_graph_out_degrees(blest_graph g, uint32_t* deg, int host) {
+    API_BEGIN
+    NEED(g && deg, "null argument");
+    const uint32_t n = g->g.n;
+    if (!n) return BLEST_OK;
+    if (host) {
+        DevBuf<uint32_t> d(n);
+        graph_out_degrees(g->g, d.p);
+        CK(cudaMemcpyAsync(deg, d.p, (size_t)n * 4, cudaMemcpyDeviceToHost, stream()));
+        CK(cudaStreamSynchronize(stream()));
+    } else {
+        graph_out_degrees(g->g, deg);
+    }
+    API_END
+}
+
+namespace blestgpu {
+__global__ void k_traversed(const uint64_t* off, const uint32_t* L, uint32_t n, unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+        if (L[v] != kInf) acc += off[v + 1] - off[v];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+}  // namespace blestgpu
+
+int blest_graph_traversed_edges(blest_graph g, const uint32_t* levels_dev, uint64_t* edges) {
+    API_BEGIN
+    NEED(g && levels_dev && edges, "null argument");
+    DevBuf<unsigned long long> acc(1);
+    CK(cudaMemsetAsync(acc.p, 0, 8, stream()));
+    if (g->g.n) {
+        k_traversed<<<grid_for(g->g.n, 256), 256, 0, stream()>>>(g->g.off.p, levels_dev, g->g.n, acc.p);
+        CK(cudaGetLastError());
+    }
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, acc.p, 8, cudaMemcpyDeviceToHost, stream()));
+    CK(cudaStreamSynchronize(stream()));
+    *edges = h / 2;
+    API_END
+}
+
+int blest_graph_free(blest_graph g) {
+    API_BEGIN
+    delete g;
+    API_END
+}
+
+// ---- ordering ---------------------------------------------------------------------------
+int blest_classify_social_like(blest_graph g, blest_social_report* out) {
+    API_BEGIN
+    NEED(g && out, "null argument");
+    const SocialReport r = classify_social_like(g->g);
+    out->top1_share = r.top1_share;
+    out->top10_share = r.top10_share;
+    out->power_law_slope = r.power_law_slope;
+    out->power_law_fit_r2 = r.power_law_fit_r2;
+    out->is_social_like = r.is_social_like;
+    out->heavy_tail_fired = r.heavy_tail;
+    out->power_law_fired = r.power_law;
+    API_END
+}
+
+int blest_order_rcm(blest_graph g, uint32_t* forward) {
+    API_BEGIN
+    NEED(g && (forward || g->g.n == 0), "null argument");
+    const auto f = rcm_forward(g->g);
+    std::memcpy(forward, f.data(), f.size() * 4);
+    API_END
+}
+
+int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint32_t* forward) {
+    API_BEGIN
+    NEED(g && (forward || g->g.n == 0), "null argument");
+    if (sigma == 0 || w == 0 || w % sigma != 0)
+        throw InvalidArgument("window size must be a positive multiple of sigma");
+    jaccard_windows_forward(g->g, sigma, w, forward);
+    API_END
+}
+
+int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward) {
+    API_BEGIN
+    NEED(forward || n == 0, "null argument");
+    const auto f = random_order_forward(n, seed);
+    std::memcpy(forward, f.data(), f.size() * 4);
+    API_END
+}
+
+int blest_relabel_permutation(uint32_t n, uint64_t seed, uint32_t* forward, int host) {
+    API_BEGIN
+    NEED(forward || n == 0, "null argument");
+    require_device();
+    if (host) {
+        DevBuf<uint32_t> f(n ? n : 1);
+        relabel_permutation(n, seed, f.p);
+        if (n) CK(cudaMemcpy(forward, f.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    } else {
+        relabel_permutation(n, seed, forward);
+    }
+    API_END
+}
+
+int blest_pick_sources(blest_graph g, uint32_t count, uint64_t seed, int skip_isolated, uint32_t* out) {
+    API_BEGIN
+    NEED(g && (out || count == 0), "null argument");
+    const auto s = pick_sources(g->g, count, seed, skip_isolated != 0);
+    std::memcpy(out, s.data(), s.size() * 4);
+    API_END
+}
+
+// ---- BVSS -------------------------------------------------------------------------------
+int blest_bvss_build(blest_graph g, blest_bvss* out) {
+    API_BEGIN
+    NEED(g && out, "null argument");
+    auto h = std::make_unique<blest_bvss_s>();
+    h->b = bvss_build(g->g);
+    *out = h.release();
+    API_END
+}
+
+int blest_bvss_upload(uint32_t n, uint64_t m, uint32_t num_vss, const uint32_t* rp, const uint32_t* v2r,
+                      const uint32_t* rows, const uint32_t* masks, int host, blest_bvss* out) {
+    API_BEGIN
+    NEED(out && rp, "null argument");
+    NEED(num_vss == 0 || (v2r && rows && masks), "null BVSS arrays");
+    require_device();
+    auto h = std::make_unique<blest_bvss_s>();
+    h->b = bvss_upload(n, m, num_vss, rp, v2r, rows, masks, host != 0);
+    *out = h.release();
+    API_END
+}
+
+int blest_bvss_get_info(blest_bvss b, blest_bvss_info* out) {
+    API_BEGIN
+    NEED(b && out, "null argument");
+    out->n = b->b.n;
+    out->m = b->b.m;
+    out->num_slice_sets = b->b.num_sets;
+    out->num_vss = b->b.num_vss;
+    out->num_unpadded_slices = b->b.num_unpadded;
+    out->sigma = kSigma;
+    out->tau = kTau;
+    API_END
+}
+
+int blest_bvss_download(blest_bvss b, uint32_t* rp, uint32_t* v2r, uint32_t* rows, uint32_t* masks) {
+    API_BEGIN
+    NEED(b, "null argument");
+    const DeviceBvss& x = b->b;
+    cudaStream_t st = stream();
+    if (rp) CK(cudaMemcpyAsync(rp, x.real_ptrs.p, ((size_t)x.num_sets + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (x.num_vss) {
+        if (v2r) CK(cudaMemcpyAsync(v2r, x.v2r.p, (size_t)x.num_vss * 4, cudaMemcpyDeviceToHost, st));
+        if (rows) CK(cudaMemcpyAsync(rows, x.row_ids.p, (uint64_t)x.num_vss * kTau * 4, cudaMemcpyDeviceToHost, st));
+        if (masks) CK(cudaMemcpyAsync(masks, x.masks.p, (uint64_t)x.num_vss * 32 * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    API_END
+}
+
+int blest_bvss_stats(blest_bvss b, blest_bvss_stats_t* out) {
+    API_BEGIN
+    NEED(b && out, "null argument");
+    const DeviceBvss& x = b->b;
+    std::memset(out, 0, sizeof(*out));
+    out->compression_ratio = bvss_compression_ratio(x);
+    out->update_divergence = bvss_update_divergence(x);
+    out->num_slice_sets = x.num_sets;
+    out->num_vss = x.num_vss;
+    out->num_slices_padded = (uint64_t)x.num_vss * kTau;
+    out->num_unpadded_slices = x.num_unpadded;
+    out->connectivity_bits = x.num_unpadded * kSigma;
+    out->bytes_real_ptrs = ((uint64_t)x.num_sets + 1) * 4;
+    out->bytes_virtual_to_real = (uint64_t)x.num_vss * 4;
+    out->bytes_row_ids = (uint64_t)x.num_vss * kTau * 4;
+    out->bytes_masks = (uint64_t)x.num_vss * 32 * 4;
+    const uint64_t words = ((uint64_t)x.n + 31) / 32;
+    out->bytes_dynamic = 4 * words * 4 + 2 * (uint64_t)x.num_vss * 4;  // R:src/bvss.cpp:629-632
+    out->bytes_levels = (uint64_t)x.n * 4;
+    bvss_slice_histogram(x, out->per_vss_slice_histogram);
+    API_END
+}
+
+int blest_bvss_update_divergence(blest_bvss b, double* out) {
+    API_BEGIN
+    NEED(b && out, "null argument");
+    *out = bvss_update_divergence(b->b);
+    API_END
+}
+
+int blest_bvss_free(blest_bvss b) {
+    API_BEGIN
+    delete b;
+    API_END
+}
+
+// ---- BFS --------------------------------------------------------------------------------
+namespace {
+EngineOptions to_opts(const blest_engine_config* cfg) {
+    EngineOptions o;
+    if (!cfg) return o;
+    if (cfg->mode != BLEST_MODE_EAGER && cfg->mode != BLEST_MODE_LAZY)
+        throw InvalidArgument("engine mode must be eager or lazy (resolve auto first)");
+    if (cfg->pull != BLEST_PULL_POPC && cfg->pull != BLEST_PULL_MMA) throw InvalidArgument("unknown pull variant");
+    o.mode = cfg->mode == BLEST_MODE_LAZY ? Mode::Lazy : Mode::Eager;
+    o.pull = cfg->pull == BLEST_PULL_MMA ? Pull::Mma : Pull::Popc;
+    o.max_levels = cfg->max_levels;
+    o.num_warps = cfg->num_warps;
+    o.grid_ctas = cfg->grid_ctas;
+    return o;
+}
+
+void fill_counters(const BfsOutcome& r, blest_counters* c, blest_level_trace* trace, uint32_t trace_cap) {
+    uint64_t d = 0, pushes = 0, full = 0, relaxed = 0;
+    for (const TraceRow& t : r.trace) {
+        d += t.queue_size;
+        pushes += t.queue_pushes;
+        full += t.full_atomics;
+        relaxed += t.relaxed_atomics;
+    }
+    if (c) {
+        c->vss_dequeues = d;
+        c->mma_calls = 2 * d;  // two m8n8k128 tiles per dequeued VSS (SPEC.md MMA exactness)
+        c->brs_baseline_mma_calls = 16 * d;
+        c->queue_pushes = pushes;
+        c->full_atomics = full;
+        c->relaxed_atomics = relaxed;
+        c->levels_processed = r.max_level;
+        c->num_levels = r.max_level + 1;
+        c->visited_count = r.visited;
+        c->trace_len = r.iterations;
+        c->trace_truncated = r.trace_truncated ? 1 : 0;
+    }
+    if (trace)
+        for (uint32_t i = 0; i < trace_cap && i < r.trace.size(); ++i)
+            std::memcpy(&trace[i], &r.trace[i], sizeof(blest_level_trace));
+}
+}  // namespace
+
+int blest_bfs_launch(blest_bvss b, uint32_t src, const blest_engine_config* cfg) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    b->eng().launch(src, to_opts(cfg));
+    g_launches.fetch_add(1);
+    API_END
+}
+
+int blest_bfs_finish(blest_bvss b, uint32_t* levels_out, blest_counters* counters, blest_level_trace* trace,
+                     uint32_t trace_cap) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    const BfsOutcome r = b->eng().finish(levels_out);
+    fill_counters(r, counters, trace, trace_cap);
+    API_END
+}
+
+int blest_bfs(blest_bvss b, uint32_t src, const blest_engine_config* cfg, uint32_t* levels_out,
+              blest_counters* counters, blest_level_trace* trace, uint32_t trace_cap) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    b->eng().launch(src, to_opts(cfg));
+    g_launches.fetch_add(1);
+    const BfsOutcome r = b->eng().finish(levels_out);
+    fill_counters(r, counters, trace, trace_cap);
+    API_END
+}
+
+int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels) {
+    API_BEGIN
+    NEED(b && levels, "null argument");
+    *levels = b->eng().levels_device();
+    API_END
+}
+
+int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    if (ctas) *ctas = b->eng().last_grid_ctas();
+    if (threads) *threads = b->eng().last_threads();
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// Shared device/host helpers for the BLEST B200 library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#if !defined(__CUDA_ARCH__) || __CUDA_ARCH__ >= 1000
+#else
+#error "libblest_b200 targets sm_100a only"
+#endif
+
+namespace blestgpu {
+
+constexpr uint32_t kInf = 0xFFFFFFFFu;  // kUnreached (R:include/blest/graph.hpp:20)
+constexpr uint32_t kSigma = 8;          // slice width (R:src/bvss.cpp:14-17)
+constexpr uint32_t kTau = 128;          // slots per VSS (BvssConfig::tau, R:include/blest/bvss.hpp:19-21)
+
+// Error classes mirror the reference's exception types (SURVEY §8(b) "Errors").
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct RuntimeError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct LogicError : std::logic_error {
+    using std::logic_error::logic_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                        std::to_string(line) + ")");
+}
+#define CK(x) ::blestgpu::cuda_check((x), #x, __FILE__, __LINE__)
+
+// The library-wide stream (set through blest_set_stream; default = legacy stream 0).
+cudaStream_t stream();
+void set_stream(cudaStream_t s);
+int num_sms();
+
+// RAII device buffer.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count) { o.p = nullptr; o.count = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; count = o.count; o.p = nullptr; o.count = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n) {
+        release();
+        count = n;
+        if (n) CK(cudaMalloc(&p, n * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    size_t bytes() const { return count * sizeof(T); }
+};
+
+inline unsigned grid_for(uint64_t work, unsigned threads, unsigned cap_blocks = 0) {
+    uint64_t b = (work + threads - 1) / threads;
+    if (b == 0) b = 1;
+    const uint64_t cap = cap_blocks ? cap_blocks : static_cast<uint64_t>(num_sms()) * 32;
+    return static_cast<unsigned>(b < cap ? b : cap);
+}
+
+#ifdef __CUDACC__
+// Streaming loads for the read-once BVSS arrays: non-coherent path, no L1 allocation,
+// L2 evict-first policy so the hot state (levels / bitmaps / queues) keeps its lines.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Sense-free generation barrier across the co-resident (cooperatively launched) grid.
+// bar[0] = arrival count, bar[1] = generation. Thread 0 of each CTA arrives; the last
+// arrival resets the count and bumps the generation (release); the rest spin with
+// acquire loads. __syncthreads on both sides orders the CTA's other threads.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = gen;
+        __threadfence();
+        const unsigned arrived = atomicAdd(&bar[0], 1u);
+        if (arrived == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar[1]), "r"(g + 1) : "memory");
+        } else {
+            while (ld_acquire_gpu(&bar[1]) == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    gen += 1;
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+    const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+#endif
+
+}  // namespace blestgpu

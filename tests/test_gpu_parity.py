@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the golden fixtures.
+Bit-exact throughout: graph CSR, BVSS arrays, level arrays, per-level queue sizes /
+discoveries / pushes (deterministic per SPEC.md:456)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2512_21967_b200 as B
+
+pytestmark = pytest.mark.gpu
+INF = 0xFFFFFFFF
+VARIANTS = [("eager", "popc"), ("eager", "mma"), ("lazy", "popc"), ("lazy", "mma")]
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.digest()
+
+
+def run(b, src, mode, pull, **kw):
+    cfg = B.EngineConfig(pull=pull, **kw)
+    return (B.run_lazy if mode == "lazy" else B.run_eager)(b, src, cfg)
+
+
+def trace_cols(cnt):
+    return np.array([[t.level, t.queue_size, t.frontier_population, t.discovered, t.queue_pushes]
+                     for t in cnt.trace], np.uint64).reshape(-1, 5)
+
+
+def check_identities(res, cnt, n):
+    """R:tests/bfs_engine_test.cpp:27-48."""
+    assert cnt.mma_calls == 2 * cnt.vss_dequeues
+    assert cnt.brs_baseline_mma_calls == 16 * cnt.vss_dequeues
+    assert sum(t.queue_pushes for t in cnt.trace) == cnt.queue_pushes
+    assert sum(t.queue_size for t in cnt.trace) == cnt.vss_dequeues
+    assert sum(t.discovered for t in cnt.trace) + 1 == res.visited_count
+    assert res.num_levels == cnt.levels_processed + 1
+    assert len(res.levels) == n
+
+
+def test_device_is_b200():
+    info = B.device_info()
+    assert info["cc"].startswith("10."), info
+
+
+def test_graph_from_edges_matches_oracle(oracle, golden):
+    f = golden("engine_families.npz")
+    for name in f["names"]:
+        name = str(name)
+        n = int(f[name + "/n"][0])
+        off, tgt = f[name + "/offsets"], f[name + "/targets"]
+        src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(off).astype(np.int64))
+        g = B.Graph.from_edges(n, (src, tgt), directed=True)
+        o, t = g.csr()
+        assert np.array_equal(o, off) and np.array_equal(t, tgt), name
+        g2 = B.Graph.from_csr(n, off, tgt)
+        assert np.array_equal(g2.csr()[1], tgt)
+    # undirected mirroring, self-loops and duplicates (R:src/graph.cpp:35-46)
+    e = np.array([[0, 1], [1, 0], [2, 2], [1, 3], [1, 3]], np.uint32)
+    g = B.Graph.from_edges(4, e, directed=False)
+    o, t = g.csr()
+    want = oracle.from_edges(4, e[:, 0], e[:, 1], directed=False)
+    assert np.array_equal(o, want.offsets) and np.array_equal(t, want.targets)
+    with pytest.raises(ValueError):
+        B.Graph.from_edges(3, np.array([[0, 5]]))
+
+
+def test_generators_match_oracle(oracle, golden):
+    gz = golden("generators.npz")
+    for scale in (8, 10, 12):
+        g = B.Graph.generate_rmat(scale, 16, 1)
+        o, t = g.csr()
+        assert sha(o, t) == bytes(gz[f"rmat{scale}/graph_sha"]), scale
+    s, d = oracle.gen_urand(1000, 16000, 3)
+    g = B.Graph.generate_urand(1000, 16000, 3)
+    want = oracle.from_edges(1000, s, d, directed=False)
+    o, t = g.csr()
+    assert np.array_equal(o, want.offsets) and np.array_equal(t, want.targets)
+    s, d = oracle.gen_grid(37, 53)
+    g = B.Graph.generate_grid(37, 53)
+    want = oracle.from_edges(37 * 53, s, d, directed=False)
+    assert np.array_equal(g.csr()[1], want.targets)
+    assert np.array_equal(B.relabel_permutation(1000, 7).forward_map(), gz["relabel1000"])
+
+
+def test_apply_permutation_matches_oracle(oracle):
+    s, d = oracle.gen_rmat(11, 8, 9)
+    g = B.Graph.from_edges(1 << 11, (s, d), directed=False)
+    f = oracle.random_relabel(1 << 11, 3)
+    h = B.apply_permutation(g, B.Permutation(f))
+    o, t = g.csr()
+    want = oracle.apply_permutation(oracle.Csr(1 << 11, o, t), f)
+    ho, ht = h.csr()
+    assert np.array_equal(ho, want.offsets) and np.array_equal(ht, want.targets)
+
+
+def test_bvss_kats(golden):
+    """R:tests/bvss_test.cpp:39-109: byte-identical arrays from the GPU builder."""
+    k = golden("bvss_kats.npz")
+    for name in sorted({key.split("/")[0] for key in k.files}):
+        n = int(k[name + "/n"][0])
+        e = k[name + "/edges"]
+        g = B.Graph.from_edges(n, e, directed=True)
+        b = B.build_bvss(g)
+        rp, v2r, rows, masks = b.arrays()
+        assert np.array_equal(rp, k[name + "/real_ptrs"]), name
+        assert np.array_equal(v2r, k[name + "/v2r"]), name
+        assert np.array_equal(rows, k[name + "/row_ids"]), name
+        assert np.array_equal(masks, k[name + "/masks"]), name
+
+
+@pytest.mark.parametrize("mode,pull", VARIANTS)
+def test_engine_families(golden, mode, pull):
+    """R:tests/bfs_engine_test.cpp:163-203: levels equal the reference; per-level queue sizes,
+    discoveries and pushes equal the reference engines' traces."""
+    f = golden("engine_families.npz")
+    for name in f["names"]:
+        name = str(name)
+        n = int(f[name + "/n"][0])
+        off, tgt = f[name + "/offsets"], f[name + "/targets"]
+        g = B.Graph.from_csr(n, off, tgt, directed=True)
+        b = B.build_bvss(g)
+        rp, v2r, rows, masks = b.arrays()
+        assert sha(rp, v2r, rows, masks) == bytes(f[name + "/bvss_sha"]), name
+        assert B.compression_ratio(b) == f[name + "/compression"][0]
+        assert b.update_divergence() == f[name + "/divergence"][0]
+        for i, s in enumerate(f[name + "/sources"]):
+            res, cnt = run(b, int(s), mode, pull)
+            assert np.array_equal(res.levels, f[f"{name}/levels{i}"]), (name, i)
+            ref = f[f"{name}/trace{i}_{1 if mode == 'lazy' else 0}"]
+            assert np.array_equal(trace_cols(cnt), ref[:, [0, 1, 2, 3, 7]]), (name, i)
+            check_identities(res, cnt, n)
+
+
+def test_init_state_and_worked_pull():
+    """R:tests/bfs_engine_test.cpp:69-97 and :116-144."""
+    e = [(17, 3), (19, 3), (22, 3)] + [(0, r) for r in range(64, 322)]
+    g = B.Graph.from_edges(384, np.array(e), directed=True)
+    b = B.build_bvss(g)
+    st = B.init_state(b, 17, B.EngineMode.Eager)
+    assert st.levels[17] == 0 and (st.levels == INF).sum() == 383
+    for mode, pull in VARIANTS:
+        res, cnt = run(b, 17, mode, pull)
+        assert res.levels[17] == 0 and res.levels[3] == 1 and res.visited_count == 2
+        assert len(cnt.trace) == 2
+        assert cnt.trace[0].queue_size == 1 and cnt.trace[0].queue_pushes == 3
+        assert cnt.trace[0].frontier_population == 1
+        assert cnt.trace[1].queue_size == 3 and cnt.trace[1].discovered == 0
+        assert cnt.mma_calls == 8 and cnt.vss_dequeues == 4 and cnt.brs_baseline_mma_calls == 64
+        assert cnt.levels_processed == 1
+
+
+def test_chain_diamond_and_empty_start():
+    """R:tests/bfs_engine_test.cpp:99-114, :146-161; empty start (SURVEY §8(a) pitfall 5)."""
+    g = B.Graph.from_edges(3, np.array([[0, 1], [1, 2]]), directed=True)
+    b = B.build_bvss(g)
+    g5 = B.Graph.from_edges(5, np.array([[0, 1], [0, 2], [1, 3], [2, 3], [3, 4]]), directed=True)
+    b5 = B.build_bvss(g5)
+    for mode, pull in VARIANTS:
+        res, cnt = run(b, 0, mode, pull)
+        assert list(res.levels) == [0, 1, 2] and res.num_levels == 3
+        assert cnt.levels_processed == 2 and len(cnt.trace) == 3 and cnt.trace[-1].discovered == 0
+        res, cnt = run(b5, 0, mode, pull, num_warps=4)
+        assert list(res.levels) == [0, 1, 1, 2, 3]
+        assert [t.queue_pushes for t in cnt.trace] == [1, 1, 1, 0]
+        # vertex 2 has no out-edges into any slice: src 2's set (set 0) has VSSs, but
+        # a sink-only graph gives an empty start
+    g = B.Graph.from_edges(16, np.array([[0, 1]]), directed=True)
+    b = B.build_bvss(g)
+    res, cnt = B.run_eager(b, 9)
+    assert res.visited_count == 1 and len(cnt.trace) == 0 and res.levels[9] == 0
+
+
+def test_errors_and_level_cap():
+    """R:tests/bfs_engine_test.cpp:308-315 and bfs source range (R:src/bfs_engine.cpp:31)."""
+    s = np.arange(15, dtype=np.uint32)
+    g = B.Graph.from_edges(16, (s, s + 1), directed=False)
+    b = B.build_bvss(g)
+    for mode, pull in VARIANTS:
+        with pytest.raises(RuntimeError):
+            run(b, 0, mode, pull, max_levels=2)
+    with pytest.raises(ValueError):
+        B.run_eager(b, 16)
+    # the engine still works after an error
+    res, _ = B.run_lazy(b, 0)
+    assert list(res.levels) == list(range(16))
+
+
+@pytest.mark.parametrize("warps", [1, 7, 32, 128, 0])
+def test_warp_count_invariance(warps):
+    """R:tests/bfs_engine_test.cpp:246-289: results invariant across warp counts."""
+    g = B.Graph.generate_rmat(12, 8, 4)
+    b = B.build_bvss(g)
+    base, bc = B.run_eager(b, 5, B.EngineConfig(num_warps=1))
+    for mode, pull in VARIANTS:
+        res, cnt = run(b, 5, mode, pull, num_warps=warps)
+        assert np.array_equal(res.levels, base.levels)
+        assert cnt.vss_dequeues == bc.vss_dequeues and cnt.queue_pushes == bc.queue_pushes
+
+
+def test_c1_rmat16_sixteen_sources(oracle):
+    """BASELINE config 1: RMAT scale 16, edgefactor 16, 16 sources, levels bit-exact against the
+    reference BFS (oracle restatement; compiled reference too when present), identity order,
+    both engines and both pull variants; counters equal the reference engine's."""
+    g = B.Graph.generate_rmat(16, 16, 1)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    srcs = g.pick_sources(16, 1)
+    want, _ = oracle.reference_bfs_many(csr, srcs)
+    b = B.build_bvss(g)
+    ob = oracle.build_bvss(csr)
+    rp, v2r, rows, masks = b.arrays()
+    assert np.array_equal(rows, ob.row_ids) and np.array_equal(masks, ob.masks)
+    for k, s in enumerate(srcs):
+        o_eng = oracle.run_engine(ob, int(s), False)
+        for mode, pull in VARIANTS:
+            res, cnt = run(b, int(s), mode, pull)
+            assert np.array_equal(res.levels, want[k]), (int(s), mode, pull)
+            assert cnt.vss_dequeues == o_eng.counters["vss_dequeues"]
+            assert cnt.queue_pushes == o_eng.counters["queue_pushes"]
+            assert np.array_equal(trace_cols(cnt)[:, [1, 3, 4]], o_eng.trace[:, [1, 3, 7]])
+    if oracle.ref_available():
+        s, d = oracle.gen_rmat(16, 16, 1)
+        rg = oracle.ref_from_edges(1 << 16, s, d, directed=False)
+        for k, src in enumerate(srcs[:4]):
+            assert np.array_equal(rg.reference_bfs(int(src))[0], want[k])
+
+
+def test_auto_pipeline_maps_levels_back(oracle):
+    """R:tests/bfs_engine_test.cpp:205-222: run_auto levels (original ids) equal the reference
+    for random, RCM and Jaccard-window orderings."""
+    g = B.Graph.generate_rmat(13, 16, 2)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    for strat in (B.OrderingStrategy.JaccardWindows, B.OrderingStrategy.Rcm,
+                  B.OrderingStrategy.Random, B.OrderingStrategy.Identity):
+        cfg = B.AutoConfig(ordering=B.SelectDefaults(window_size=1 << 10, force=strat), seed=3)
+        b, plan = B.prepare(g, cfg)
+        for src in g.pick_sources(3, 11):
+            r = B.run_auto_prebuilt(b, plan, int(src), cfg)
+            assert np.array_equal(r.bfs.levels, oracle.reference_bfs(csr, int(src))[0]), strat
+            assert r.bfs.source == int(src)
