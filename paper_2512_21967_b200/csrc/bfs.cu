@@ -140,8 +140,11 @@ __device__ __forceinline__ void push_column(const Params& p, bool flag, unsigned
     if (!ball) return;
     const uint32_t k = __popc(ball);
     if (count + k > kPushCap) {
-        pushes += flush_pushes(p, buf, count, Qn, qlen_next);
-        full += 1;
+        const uint32_t t = flush_pushes(p, buf, count, Qn, qlen_next);
+        if (lane_id() == 0) {  // per-warp quantities: count once, not per lane
+            pushes += t;
+            full += 1;
+        }
     }
     if (flag) buf[count + __popc(ball & ((1u << lane_id()) - 1))] = item;
     __syncwarp();
@@ -390,8 +393,11 @@ __global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
             }
         }
         if (pcount) {
-            ctr[3] += flush_pushes(p, pbuf, pcount, Qn, qlen_next);
-            ctr[1] += 1;
+            const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next);
+            if (lane == 0) {
+                ctr[3] += t;
+                ctr[1] += 1;
+            }
         }
         level_barrier(p, sm, gen, level, ctr, true);
     }
