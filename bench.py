@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--pull", default="popc", choices=["popc", "mma"])
     ap.add_argument("--order", default=None, choices=["auto", "identity", "rcm", "jaccard", "random"])
     ap.add_argument("--window", type=int, default=1 << 16)
+    ap.add_argument("--threads", type=int, default=0, help="threads per CTA (256/512/1024; 0 = default)")
     ap.add_argument("--source-seed", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -255,10 +256,10 @@ def main():
         return
 
     ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
-                           L.PULL_MMA if args.pull == "mma" else L.PULL_POPC, 0, 0, 0)
+                           L.PULL_MMA if args.pull == "mma" else L.PULL_POPC, 0, 0, 0, args.threads)
     ctr = L.CountersT()
     # ---- census (untimed): deterministic counters + traversed edges per source ----
-    census = census_of(lib, L, b, prep, mine, lazy, args.pull)
+    census = census_of(lib, L, b, prep, mine, lazy, args.pull, args.threads)
     if args.validate:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
@@ -363,11 +364,11 @@ def main():
         dist.destroy_process_group()
 
 
-def census_of(lib, L, b, prep, sources, lazy, pull):
+def census_of(lib, L, b, prep, sources, lazy, pull, threads=0):
     """Per source: VSS dequeues D, pushes P, visited V, level iterations L and traversed
     undirected edges E (on the permuted graph, whose ids the level array uses)."""
     ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
-                           L.PULL_MMA if pull == "mma" else L.PULL_POPC, 0, 0, 0)
+                           L.PULL_MMA if pull == "mma" else L.PULL_POPC, 0, 0, 0, threads)
     ctr = L.CountersT()
     lv_ptr = C.c_void_p()
     out = []

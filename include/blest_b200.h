@@ -140,6 +140,7 @@ typedef struct {
     uint32_t max_levels;   /* 0 = n + 1 */
     uint32_t num_warps;    /* logical warps for the round-robin VSS split; 0 = whole grid */
     uint32_t grid_ctas;    /* 0 = persistent grid (all co-resident CTAs) */
+    uint32_t threads_per_cta; /* 256, 512 or 1024; 0 = default (512) */
 } blest_engine_config;
 /* EngineCounters (R:include/blest/bfs_engine.hpp:39-50) + BfsResult scalars (graph.hpp:111-116). */
 typedef struct {
@@ -167,6 +168,9 @@ int blest_bfs(blest_bvss b, uint32_t src, const blest_engine_config* cfg, uint32
 int blest_bfs_launch(blest_bvss b, uint32_t src, const blest_engine_config* cfg);
 int blest_bfs_finish(blest_bvss b, uint32_t* levels_out, blest_counters* counters,
                      blest_level_trace* trace_out, uint32_t trace_cap);
+/* Per-level device timestamps of the last finished run (%globaltimer ns, 3 per level:
+ * level start, lazy stage-1 end, level end); *rows = levels recorded. */
+int blest_bfs_phase_times(blest_bvss b, uint64_t* out, uint32_t cap, uint32_t* rows);
 /* Device pointer to the level array of the last run on b (n entries). */
 int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
 /* Launch geometry of the last run (CTAs, threads per CTA). */

@@ -58,7 +58,7 @@ class SocialReportT(C.Structure):
 
 class EngineConfigT(C.Structure):
     _fields_ = [("mode", C.c_int), ("pull", C.c_int), ("max_levels", C.c_uint32),
-                ("num_warps", C.c_uint32), ("grid_ctas", C.c_uint32)]
+                ("num_warps", C.c_uint32), ("grid_ctas", C.c_uint32), ("threads_per_cta", C.c_uint32)]
 
 
 class CountersT(C.Structure):
@@ -113,6 +113,7 @@ SIGNATURES = {
     "blest_bfs_launch": (i32, [vp, u32, P(EngineConfigT)]),
     "blest_bfs_finish": (i32, [vp, vp, P(CountersT), vp, u32]),
     "blest_bfs_levels_device": (i32, [vp, P(vp)]),
+    "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),
 }
 

@@ -460,6 +460,7 @@ class EngineConfig:
     workers: int = 1  # accepted for API parity; the GPU grid replaces CPU workers
     pull: str = "popc"  # "popc" (CUDA-core) or "mma" (b1 m8n8k128 mma.sync tile)
     grid_ctas: int = 0
+    threads_per_cta: int = 0
 
 
 @dataclass
@@ -526,7 +527,7 @@ def _cfg_struct(cfg: EngineConfig, mode: EngineMode) -> L.EngineConfigT:
         raise ValueError("pull must be 'popc' or 'mma'")
     return L.EngineConfigT(L.MODE_LAZY if mode == EngineMode.Lazy else L.MODE_EAGER,
                            L.PULL_MMA if cfg.pull == "mma" else L.PULL_POPC,
-                           cfg.max_levels, cfg.num_warps, cfg.grid_ctas)
+                           cfg.max_levels, cfg.num_warps, cfg.grid_ctas, cfg.threads_per_cta)
 
 
 def _run(b: Bvss, src: int, cfg: EngineConfig, mode: EngineMode, want_levels: bool = True):

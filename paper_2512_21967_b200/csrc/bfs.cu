@@ -16,27 +16,31 @@
 // triple-buffered: level ℓ reads F[ℓ%3] (α), atomically ORs discoveries into F[(ℓ+1)%3],
 // and zeroes the bytes of F[(ℓ+2)%3] that level ℓ-1 used (found from queue ℓ-1), so no
 // Θ(n) clear is ever needed (the reference clears all words per level, :227-228).
-// Lazy (Alg. 3, :238-350): stage 1 pulls with fire-and-forget REDs into V_next (skipped
-// when V_curr already has the bit — legal per SURVEY §8(a) pitfall 7); barrier; stage 2
-// sweeps ⌈n/32⌉ words, writes levels with coalesced 128 B stores and enqueues; barrier.
+// Enqueue: lanes append slice sets to a per-warp shared-memory buffer; a flush reserves
+// queue space with ONE atomicAdd per warp buffer and expands [real_ptrs[s], real_ptrs[s+1]).
 //
-// Enqueue (both modes): lanes append slice sets to a per-warp shared-memory buffer; a
-// flush reserves queue space with ONE atomicAdd per warp-buffer (warp-aggregated
-// reservation, PAPER §4.2) and expands each set's VSS range [real_ptrs[s], real_ptrs[s+1]).
-#include <cooperative_groups.h>
-
+// Lazy (Alg. 3, :238-350): visited words are interleaved {V_curr, V_next} so one 8-byte
+// load answers "visited before this level, or already marked this level?"; only then a
+// fire-and-forget RED sets the V_next bit (stage 1, :286-289). Stage 2 (:296-338) gives
+// every CTA one contiguous chunk of words: pass A computes diff = V_next & ~V_curr,
+// writes levels with coalesced 128 B stores, and counts the VSSs to enqueue; the CTA
+// publishes its count and sums its predecessors' (tagged with the level, so no reset);
+// pass B writes its slice sets' VSS ranges at that offset. The next queue is therefore in
+// ascending slice-set order — deterministic, and stage 1 then streams the BVSS in address
+// order — with no contended queue-tail atomic at all.
 #include <algorithm>
+#include <atomic>
 
 #include "bfs.cuh"
 
 namespace blestgpu {
 
+extern std::atomic<uint64_t> g_launches;
+
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarpsPerCta = kThreads / 32;
 constexpr int kBatch = 4;         // VSSs in flight per warp
-constexpr int kPushCap = 64;      // per-warp push buffer entries
+constexpr int kPushCap = 64;      // per-warp push buffer entries (eager)
 constexpr unsigned long long kNoEntry = ~0ull;
 
 struct Params {
@@ -46,31 +50,42 @@ struct Params {
     const uint32_t* __restrict__ masks;
     const uint4* __restrict__ rows4;
     uint32_t* L;
-    uint32_t* B0;  // eager F0 / lazy V_curr
-    uint32_t* B1;  // eager F1 / lazy V_next
-    uint32_t* B2;  // eager F2
+    uint32_t* B0;  // eager F0 | lazy V (uint2 {cur, next}, spans B0..B1)
+    uint32_t* B1;  // eager F1
+    uint32_t* B2;  // eager F2 | lazy per-level diff
     unsigned long long* Q0;
     unsigned long long* Q1;
     unsigned long long* Q2;
     unsigned long long* ctl;    // [0..3] qlen ring, [4] iterations, [5] max level, [6] status
+    unsigned long long* agg;    // lazy stage 2: per-CTA (level << 40 | count)
     unsigned* bar;
     unsigned long long* trace;
+    unsigned long long* tstamp;  // per level: [start, stage-1 end, level end] (%globaltimer ns)
     uint32_t trace_cap;
     uint32_t src;
     uint32_t cap;
     uint32_t num_warps;
 };
 
+template <int THREADS>
 struct Smem {
-    unsigned long long push[kWarpsPerCta][kPushCap];  // ss | aux << 32
-    unsigned long long ctr[4];                        // discovered, full, relaxed, pushes
+    unsigned long long push[THREADS / 32][kPushCap];  // eager: ss | ss << 32
+    unsigned long long ctr[4];                         // discovered, full, relaxed, pushes
+    unsigned long long red[THREADS / 32];              // block reductions / scans
+    unsigned long long base;
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Fire-and-forget OR (REDG): the lazy scheme's "relaxed atomic" (R:src/bfs_engine.cpp:287-288).
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
-    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
 template <int MODE>
@@ -87,8 +102,33 @@ __device__ __forceinline__ uint32_t* fbuf(const Params& p, uint32_t idx) {
     return k == 0 ? p.B0 : (k == 1 ? p.B1 : p.B2);
 }
 
-// Warp flush: reserve room for the buffered slice sets' VSS ranges with one atomicAdd and
-// write the expanded entries. Returns VSS entries written (for the trace).
+// Block-wide exclusive scan of a u64 per thread; returns the thread's offset, *total the sum.
+template <int THREADS>
+__device__ __forceinline__ unsigned long long block_excl_scan(Smem<THREADS>& sm, unsigned long long x,
+                                                              unsigned long long* total) {
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    unsigned long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += y;
+    }
+    __syncthreads();  // protect sm.red from a previous use
+    if (lane == 31) sm.red[warp] = incl;
+    __syncthreads();
+    unsigned long long before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < THREADS / 32; ++w) {
+        const unsigned long long t = sm.red[w];
+        if (w < (int)warp) before += t;
+        all += t;
+    }
+    *total = all;
+    return before + incl - x;
+}
+
+// Warp flush (eager): reserve room for the buffered slice sets' VSS ranges with one
+// atomicAdd and write the expanded entries. Returns VSS entries written.
 __device__ uint32_t flush_pushes(const Params& p, unsigned long long* buf, uint32_t& count,
                                  unsigned long long* Qn, unsigned long long* qlen_next) {
     const unsigned lane = lane_id();
@@ -184,9 +224,10 @@ __device__ __forceinline__ void column_counts(uint32_t m, uint32_t alpha, uint32
 }
 
 // Flush per-thread counters into the CTA's shared counters, then (thread 0) into the
-// level's trace row; then the grid barrier.
-__device__ __forceinline__ void level_barrier(const Params& p, Smem& sm, unsigned& gen, uint32_t level,
-                                              uint32_t (&c)[4], bool count_level) {
+// level's trace row; then the grid barrier; block 0 stamps the time.
+template <int THREADS>
+__device__ __forceinline__ void level_barrier(const Params& p, Smem<THREADS>& sm, unsigned& gen,
+                                              uint32_t level, uint32_t (&c)[4], int stamp_slot) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t s = warp_sum(c[i]);
@@ -194,7 +235,7 @@ __device__ __forceinline__ void level_barrier(const Params& p, Smem& sm, unsigne
         c[i] = 0;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && count_level) {
+    if (threadIdx.x == 0) {
         const uint32_t row = min(level - 1, p.trace_cap - 1);
         unsigned long long* t = p.trace + 8ull * row;
         if (sm.ctr[0]) {
@@ -208,21 +249,25 @@ __device__ __forceinline__ void level_barrier(const Params& p, Smem& sm, unsigne
         for (int i = 0; i < 4; ++i) sm.ctr[i] = 0;
     }
     grid_barrier(p.bar, gen);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
+        p.tstamp[3ull * (level - 1) + stamp_slot] = globaltimer();
 }
 
-template <int MODE, int PULL>
-__global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
-    __shared__ Smem sm;
+template <int MODE, int PULL, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
+    constexpr int WPC = THREADS / 32;
+    __shared__ Smem<THREADS> sm;
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
-    const uint64_t gtid = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
-    const uint64_t gthreads = (uint64_t)gridDim.x * kThreads;
-    const uint32_t gw = blockIdx.x * kWarpsPerCta + warp;
-    const uint32_t all_warps = gridDim.x * kWarpsPerCta;
+    const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    const uint64_t gthreads = (uint64_t)gridDim.x * THREADS;
+    const uint32_t gw = blockIdx.x * WPC + warp;
+    const uint32_t all_warps = gridDim.x * WPC;
     const uint32_t NW = (p.num_warps && p.num_warps < all_warps) ? p.num_warps : all_warps;
     unsigned gen = 0;
     const uint64_t pol = evict_first_policy();
     if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
+    uint2* V = reinterpret_cast<uint2*>(p.B0);  // lazy {cur, next}
 
     // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
     const uint32_t src = p.src;
@@ -237,8 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
             p.B1[w] = seed;  // F[1] = F_curr of level 1
             p.B2[w] = 0;
         } else {
-            p.B0[w] = seed;  // V_curr
-            p.B1[w] = seed;  // V_next
+            V[w] = make_uint2(seed, seed);
         }
     }
     {
@@ -248,6 +292,7 @@ __global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
                         : ((unsigned long long)(1u << (src & 7)) << 32);
         for (uint64_t i = gtid; i < seed_e - seed_b; i += gthreads) Q1[i] = aux | (seed_b + i);
     }
+    if (threadIdx.x == 0) p.agg[blockIdx.x] = 0;  // stage-2 tags are per run
     if (gtid == 0) {
         p.ctl[0] = 0;
         p.ctl[1] = seed_e - seed_b;
@@ -276,6 +321,7 @@ __global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
             if (level - 1 < p.trace_cap) {
                 p.trace[8ull * (level - 1) + 0] = level;
                 p.trace[8ull * (level - 1) + 1] = len;
+                p.tstamp[3ull * (level - 1)] = globaltimer();
             } else {
                 atomicAdd(&p.trace[8ull * (p.trace_cap - 1) + 1], len);
             }
@@ -286,8 +332,7 @@ __global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
         unsigned long long* Qn = queue_at<MODE>(p, level + 1);
         unsigned long long* qlen_next = &p.ctl[(level + 1) & 3];
         const uint32_t* Fc = (MODE == 0) ? fbuf(p, level) : nullptr;
-        uint32_t* Fn = (MODE == 0) ? fbuf(p, level + 1) : p.B1;
-        const uint32_t* Vc = p.B0;
+        uint32_t* Fn = (MODE == 0) ? fbuf(p, level + 1) : nullptr;
 
         if (MODE == 0) {
             // Zero the frontier bytes level ℓ-1 read: they become F_next at ℓ+1.
@@ -331,77 +376,156 @@ __global__ void __launch_bounds__(kThreads) k_bfs(Params p) {
                                                        : (uint32_t)((ej[j] >> 32) & 0xFFu);
                     uint32_t cnt[4];
                     column_counts<PULL>(mk[j], alpha, cnt);
-                    const uint32_t rr[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                    // All four dependent state loads of this VSS are issued before any of
+                    // them is consumed (4 independent L1/L2 requests in flight per lane).
+                    if (MODE == 1) {
+                        // stage-1 sink (:286-289): relaxed OR into V_next unless the vertex
+                        // was visited before this level or is already marked this level.
+                        uint2 vw[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        bool push = false;
-                        uint32_t u = rr[c];
-                        if (cnt[c]) {
-                            const uint32_t bit = 1u << (u & 31);
-                            if (MODE == 1) {
-                                // stage-1 sink (:286-289): relaxed OR into V_next
-                                if (!(Vc[u >> 5] & bit)) {
-                                    red_or(Fn + (u >> 5), bit);
-                                    ++ctr[2];
-                                }
-                            } else if (p.L[u] == kInf) {  // eager sink (:198-211)
-                                const uint32_t old = atomicOr(Fn + (u >> 5), bit);
-                                ++ctr[1];
-                                if (!(old & bit)) {
-                                    p.L[u] = level;
-                                    ++ctr[0];
-                                    push = ((old >> (8 * ((u >> 3) & 3))) & 0xFFu) == 0;
-                                }
+                        for (int c = 0; c < 4; ++c) vw[c] = cnt[c] ? V[u[c] >> 5] : make_uint2(~0u, ~0u);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            if (!(((vw[c].x | vw[c].y) >> (u[c] & 31)) & 1u)) {
+                                red_or(&V[u[c] >> 5].y, 1u << (u[c] & 31));
+                                ++ctr[2];
                             }
                         }
-                        if (MODE == 0)
-                            push_column(p, push, (unsigned long long)(u >> 3) << 32 | (u >> 3), pbuf,
+                    } else {
+                        // eager sink (:198-211)
+                        uint32_t lv[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) lv[c] = cnt[c] ? p.L[u[c]] : 0u;
+                        uint32_t old[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            old[c] = (lv[c] == kInf) ? atomicOr(Fn + (u[c] >> 5), 1u << (u[c] & 31))
+                                                     : 0xFFFFFFFFu;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            bool push = false;
+                            if (lv[c] == kInf) {
+                                ++ctr[1];
+                                if (!((old[c] >> (u[c] & 31)) & 1u)) {
+                                    p.L[u[c]] = level;
+                                    ++ctr[0];
+                                    push = ((old[c] >> (8 * ((u[c] >> 3) & 3))) & 0xFFu) == 0;
+                                }
+                            }
+                            push_column(p, push, (unsigned long long)(u[c] >> 3) << 32 | (u[c] >> 3), pbuf,
                                         pcount, Qn, qlen_next, ctr[3], ctr[1]);
+                        }
                     }
                 }
             }
         }
 
         if (MODE == 1) {
-            level_barrier(p, sm, gen, level, ctr, true);
-            // ---- stage 2 (R:src/bfs_engine.cpp:296-338): word sweep ----
-            uint32_t* Vn = p.B1;
-            uint32_t* Vcw = p.B0;
-            for (uint64_t wb = (uint64_t)gw * 32; wb < p.words; wb += (uint64_t)all_warps * 32) {
-                const uint64_t w = wb + lane;
-                uint32_t diff = 0, nx = 0;
-                if (w < p.words) {
-                    nx = Vn[w];
-                    diff = nx & ~Vcw[w];
-                    if (diff) Vcw[w] = nx;
+            level_barrier<THREADS>(p, sm, gen, level, ctr, 1);
+            // ---- stage 2 (R:src/bfs_engine.cpp:296-338): chunked word sweep ----
+            uint32_t* Fd = p.B2;  // this level's diff words (the reference's F_curr, :310-311)
+            const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
+            const uint64_t w0 = (uint64_t)blockIdx.x * per;
+            const uint64_t w1 = min(w0 + per, p.words);
+            unsigned long long mine = 0;
+            // pass A: diff, V_curr update, levels, VSS count of the sets to enqueue
+            for (uint64_t wb = w0; wb < w1; wb += THREADS) {
+                const uint64_t w = wb + threadIdx.x;
+                uint32_t diff = 0;
+                if (w < w1) {
+                    const uint2 v = V[w];
+                    diff = v.y & ~v.x;
+                    Fd[w] = diff;
+                    if (diff) V[w].x = v.y;
+                    for (uint32_t d = diff; d; ) {
+                        const int bsel = (__ffs(d) - 1) >> 3;
+                        d &= ~(0xFFu << (8 * bsel));
+                        const uint64_t ss = 4 * w + bsel;
+                        mine += p.rp[ss + 1] - p.rp[ss];
+                    }
                 }
                 ctr[0] += __popc(diff);
+                const uint64_t wwarp = wb + 32 * warp;  // this warp's 32 words
                 unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
                 while (ball) {
                     const int k = __ffs(ball) - 1;
                     ball &= ball - 1;
                     const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
-                    if ((dk >> lane) & 1u) p.L[32 * (wb + k) + lane] = level;
-                }
-#pragma unroll
-                for (int bsel = 0; bsel < 4; ++bsel) {
-                    const uint32_t alpha = (diff >> (8 * bsel)) & 0xFFu;
-                    const uint64_t ss = 4 * w + bsel;
-                    push_column(p, alpha != 0, (unsigned long long)alpha << 32 | ss, pbuf, pcount, Qn,
-                                qlen_next, ctr[3], ctr[1]);
+                    if ((dk >> lane) & 1u) p.L[32 * (wwarp + k) + lane] = level;
                 }
             }
+            unsigned long long cta_total = 0;
+            block_excl_scan<THREADS>(sm, mine, &cta_total);
+            // publish this CTA's count, then sum the predecessors' (level-tagged)
+            if (threadIdx.x == 0) {
+                const unsigned long long tag = ((unsigned long long)level << 40) | cta_total;
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag) : "memory");
+            }
+            if (warp == 0) {
+                unsigned long long before = 0;
+                for (uint32_t c = lane; c < blockIdx.x; c += 32) {
+                    unsigned long long x;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
+                    } while ((x >> 40) != level);
+                    before += x & ((1ull << 40) - 1);
+                }
+                before = warp_sum(before);
+                if (lane == 0) {
+                    sm.base = before;
+                    if (blockIdx.x == gridDim.x - 1) *qlen_next = before + cta_total;
+                }
+            }
+            __syncthreads();
+            // pass B: expand the chunk's slice sets into the queue, in slice-set order
+            unsigned long long running = sm.base;
+            for (uint64_t wb = w0; wb < w1; wb += THREADS) {
+                const uint64_t w = wb + threadIdx.x;
+                const uint32_t diff = (w < w1) ? Fd[w] : 0u;
+                uint32_t b[4], e[4];
+                unsigned long long cnt = 0;
+#pragma unroll
+                for (int bsel = 0; bsel < 4; ++bsel) {
+                    b[bsel] = e[bsel] = 0;
+                    if ((diff >> (8 * bsel)) & 0xFFu) {
+                        const uint64_t ss = 4 * w + bsel;
+                        b[bsel] = p.rp[ss];
+                        e[bsel] = p.rp[ss + 1];
+                        cnt += e[bsel] - b[bsel];
+                    }
+                }
+                unsigned long long it_total = 0;
+                unsigned long long pos = running + block_excl_scan<THREADS>(sm, cnt, &it_total);
+#pragma unroll
+                for (int bsel = 0; bsel < 4; ++bsel) {
+                    const unsigned long long aux = (unsigned long long)((diff >> (8 * bsel)) & 0xFFu) << 32;
+                    for (uint32_t v = b[bsel]; v < e[bsel]; ++v) Qn[pos++] = aux | v;
+                }
+                running += it_total;
+            }
+            if (threadIdx.x == 0) ctr[3] += (uint32_t)cta_total;
         }
-        if (pcount) {
+        if (MODE == 0 && pcount) {
             const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next);
             if (lane == 0) {
                 ctr[3] += t;
                 ctr[1] += 1;
             }
         }
-        level_barrier(p, sm, gen, level, ctr, true);
+        level_barrier<THREADS>(p, sm, gen, level, ctr, 2);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
+}
+
+template <int MODE, int PULL>
+void* pick_kernel(int threads) {
+    switch (threads) {
+        case 256: return (void*)k_bfs<MODE, PULL, 256>;
+        case 512: return (void*)k_bfs<MODE, PULL, 512>;
+        case 1024: return (void*)k_bfs<MODE, PULL, 1024>;
+    }
+    throw InvalidArgument("threads per CTA must be 256, 512 or 1024");
 }
 
 }  // namespace
@@ -414,8 +538,11 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     bits_.alloc(3 * (words_ ? words_ : 1));
     q_.alloc(3 * (uint64_t)(b.num_vss ? b.num_vss : 1));
     ctl_.alloc(8);
+    agg_.alloc(4096);
+    CK(cudaMemset(agg_.p, 0, 4096 * 8));
     bar_.alloc(2);
     trace_.alloc(8ull * trace_cap_);
+    tstamp_.alloc(3ull * trace_cap_);
     CK(cudaMallocHost(&pinned_, 8 * sizeof(unsigned long long)));
 }
 
@@ -425,17 +552,18 @@ BfsEngine::~BfsEngine() {
 
 void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (src >= b_.n) throw InvalidArgument("bfs source out of range");
-    const int mode = (int)opt.mode, pull = (int)opt.pull;
-    void (*kern)(Params) = nullptr;
-    if (mode == 0 && pull == 0) kern = k_bfs<0, 0>;
-    else if (mode == 0 && pull == 1) kern = k_bfs<0, 1>;
-    else if (mode == 1 && pull == 0) kern = k_bfs<1, 0>;
-    else kern = k_bfs<1, 1>;
+    const int threads = opt.threads ? (int)opt.threads : 512;
+    void* kern = nullptr;
+    if (opt.mode == Mode::Eager)
+        kern = opt.pull == Pull::Mma ? pick_kernel<0, 1>(threads) : pick_kernel<0, 0>(threads);
+    else
+        kern = opt.pull == Pull::Mma ? pick_kernel<1, 1>(threads) : pick_kernel<1, 0>(threads);
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
     if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
     uint32_t ctas = (uint32_t)per_sm * (uint32_t)num_sms();
     if (opt.grid_ctas && opt.grid_ctas < ctas) ctas = opt.grid_ctas;
+    if (ctas > agg_.count) ctas = (uint32_t)agg_.count;
     Params p{};
     p.n = b_.n;
     p.num_sets = b_.num_sets;
@@ -452,8 +580,10 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.Q1 = q_.p + qcap;
     p.Q2 = q_.p + 2 * qcap;
     p.ctl = ctl_.p;
+    p.agg = agg_.p;
     p.bar = bar_.p;
     p.trace = trace_.p;
+    p.tstamp = tstamp_.p;
     p.trace_cap = trace_cap_;
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
@@ -461,9 +591,10 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     cudaStream_t st = stream();
     CK(cudaMemsetAsync(bar_.p, 0, 2 * sizeof(unsigned), st));
     void* args[] = {&p};
-    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(ctas), dim3(kThreads), args, 0, st));
+    CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, 0, st));
+    g_launches.fetch_add(1);
     last_ctas_ = ctas;
-    last_threads_ = kThreads;
+    last_threads_ = threads;
     last_src_ = src;
     last_mode_ = opt.mode;
     launched_ = true;
@@ -493,6 +624,9 @@ BfsOutcome BfsEngine::finish(uint32_t* levels_host) {
         r.stage1_full_atomics = (last_mode_ == Mode::Eager) ? r.full_atomics : 0;
     }
     out.visited = visited;
+    out.phase_ns.resize(3ull * rows);
+    if (rows)
+        CK(cudaMemcpy(out.phase_ns.data(), tstamp_.p, 3ull * rows * 8, cudaMemcpyDeviceToHost));
     if (runaway)
         throw RuntimeError("BFS ran past the level safety cap at level " +
                            std::to_string(out.iterations + 1) + " — engine invariant broken");

@@ -18,6 +18,7 @@ struct EngineOptions {
     uint32_t max_levels = 0;  // 0 = n + 1 (R:src/bfs_engine.cpp:68-70)
     uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
+    uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
 };
 
 // One row per level, same fields as LevelTrace (R:include/blest/bfs_engine.hpp:27-37).
@@ -32,6 +33,7 @@ struct BfsOutcome {
     uint64_t visited = 0;
     bool trace_truncated = false;
     std::vector<TraceRow> trace;
+    std::vector<uint64_t> phase_ns;  // per level: start, stage-1 end (lazy), level end
 };
 
 // Per-structure device workspace; sized once, reused across sources.
@@ -62,8 +64,10 @@ private:
     DevBuf<uint32_t> bits_;              // 3 * words_
     DevBuf<unsigned long long> q_;       // 3 * max(num_vss, 1) entries
     DevBuf<unsigned long long> ctl_;     // qlen[4], result[4]
+    DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA counts
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
+    DevBuf<unsigned long long> tstamp_;  // trace_cap_ * 3
     unsigned long long* pinned_ = nullptr;  // host mirror for ctl_ readback
     uint32_t last_ctas_ = 0, last_threads_ = 0, last_src_ = 0;
     Mode last_mode_ = Mode::Eager;

@@ -20,6 +20,7 @@ struct blest_graph_s {
 struct blest_bvss_s {
     DeviceBvss b;
     std::unique_ptr<BfsEngine> engine;
+    std::vector<uint64_t> last_phase_ns;
     BfsEngine& eng() {
         if (!engine) engine = std::make_unique<BfsEngine>(b);
         return *engine;
@@ -410,6 +411,7 @@ EngineOptions to_opts(const blest_engine_config* cfg) {
     o.max_levels = cfg->max_levels;
     o.num_warps = cfg->num_warps;
     o.grid_ctas = cfg->grid_ctas;
+    o.threads = cfg->threads_per_cta;
     return o;
 }
 
@@ -444,7 +446,6 @@ int blest_bfs_launch(blest_bvss b, uint32_t src, const blest_engine_config* cfg)
     API_BEGIN
     NEED(b, "null bvss");
     b->eng().launch(src, to_opts(cfg));
-    g_launches.fetch_add(1);
     API_END
 }
 
@@ -453,7 +454,19 @@ int blest_bfs_finish(blest_bvss b, uint32_t* levels_out, blest_counters* counter
     API_BEGIN
     NEED(b, "null bvss");
     const BfsOutcome r = b->eng().finish(levels_out);
+    b->last_phase_ns = r.phase_ns;
     fill_counters(r, counters, trace, trace_cap);
+    API_END
+}
+
+int blest_bfs_phase_times(blest_bvss b, uint64_t* out, uint32_t cap, uint32_t* rows) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    const uint32_t n = (uint32_t)(b->last_phase_ns.size() / 3);
+    if (rows) *rows = n;
+    if (out)
+        for (uint32_t i = 0; i < n && i < cap; ++i)
+            for (int k = 0; k < 3; ++k) out[3 * i + k] = b->last_phase_ns[3 * i + k];
     API_END
 }
 
@@ -462,8 +475,8 @@ int blest_bfs(blest_bvss b, uint32_t src, const blest_engine_config* cfg, uint32
     API_BEGIN
     NEED(b, "null bvss");
     b->eng().launch(src, to_opts(cfg));
-    g_launches.fetch_add(1);
     const BfsOutcome r = b->eng().finish(levels_out);
+    b->last_phase_ns = r.phase_ns;
     fill_counters(r, counters, trace, trace_cap);
     API_END
 }

@@ -130,7 +130,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
             __threadfence();
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar[1]), "r"(g + 1) : "memory");
         } else {
-            while (ld_acquire_gpu(&bar[1]) == g) __nanosleep(32);
+            // relaxed spin (an acquire load per iteration would invalidate the SM's L1
+            // under the CTAs still working); one acquire fence after the exit
+            while (ld_relaxed_gpu(&bar[1]) == g) __nanosleep(32);
         }
         __threadfence();
     }
