@@ -95,6 +95,9 @@ int blest_order_rcm(blest_graph g, uint32_t* forward);
 /* jaccard_with_windows(g, sigma, w, nullptr) (R:include/blest/ordering.hpp:52-53,
  * R:src/ordering.cpp:139-166) — one CTA per window on the GPU. */
 int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint32_t* forward);
+/* Hub-first pre-pass (new; composable like R:include/blest/ordering.hpp PrePass):
+ * forward[u] = rank of (out-degree descending, id ascending). */
+int blest_order_degree(blest_graph g, uint32_t* forward, int host);
 /* random_order(n, seed) (R:include/blest/ordering.hpp:58, R:src/ordering.cpp:268-275). */
 int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward);
 /* Harness relabel: forward[i] = rank of (splitmix64(seed, i), i); host or device output. */

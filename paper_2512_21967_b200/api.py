@@ -227,6 +227,7 @@ class OrderingStrategy(enum.Enum):
 class PrePass(enum.Enum):
     None_ = "none"
     BfsLocality = "bfs-locality"
+    DegreeSort = "degree"  # B200 addition: hub-first ids (shared-memory visited cache)
 
 
 def ordering_strategy_from_string(s: str) -> OrderingStrategy:
@@ -321,7 +322,16 @@ def make_permutation(g: Graph, plan: OrderingPlan, sigma: int = 8, seed: int = 0
         return rcm(g)
     if plan.pre_pass == PrePass.BfsLocality:
         raise NotImplementedError("bfs-locality pre-pass is out of scope (SURVEY §2)")
+    if plan.pre_pass == PrePass.DegreeSort:
+        return jaccard_with_windows(g, sigma, plan.window_size, degree_order(g))
     return jaccard_with_windows(g, sigma, plan.window_size)
+
+
+def degree_order(g: Graph) -> Permutation:
+    """Hub-first pre-pass: rank by (out-degree descending, id ascending), on the GPU."""
+    f = np.zeros(max(g.num_vertices(), 1), np.uint32)
+    L.check(L.lib().blest_order_degree(g.handle, _ptr(f), 1))
+    return Permutation(f[: g.num_vertices()])
 
 
 # ------------------------------------------------------------------------------------

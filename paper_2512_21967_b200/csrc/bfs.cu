@@ -65,11 +65,15 @@ struct Params {
     uint32_t src;
     uint32_t cap;
     uint32_t num_warps;
+    uint32_t* hubV;          // lazy: copy of V_curr words [0, hub_words) (the hub prefix)
+    uint32_t hub_words;      // words staged in shared memory on dense levels (0 = off)
+    uint64_t dense_min;      // queue length from which a level stages the hub prefix
+    uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
 };
 
-template <int THREADS>
+template <int THREADS, int MODE = 0>
 struct Smem {
-    unsigned long long push[THREADS / 32][kPushCap];  // eager: ss | ss << 32
+    unsigned long long push[THREADS / 32][MODE == 0 ? kPushCap : 1];  // eager: ss | ss << 32
     unsigned long long ctr[4];                         // discovered, full, relaxed, pushes
     unsigned long long red[THREADS / 32];              // block reductions / scans
     unsigned long long base;
@@ -103,8 +107,8 @@ __device__ __forceinline__ uint32_t* fbuf(const Params& p, uint32_t idx) {
 }
 
 // Block-wide exclusive scan of a u64 per thread; returns the thread's offset, *total the sum.
-template <int THREADS>
-__device__ __forceinline__ unsigned long long block_excl_scan(Smem<THREADS>& sm, unsigned long long x,
+template <int THREADS, int MODE>
+__device__ __forceinline__ unsigned long long block_excl_scan(Smem<THREADS, MODE>& sm, unsigned long long x,
                                                               unsigned long long* total) {
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     unsigned long long incl = x;
@@ -225,8 +229,8 @@ __device__ __forceinline__ void column_counts(uint32_t m, uint32_t alpha, uint32
 
 // Flush per-thread counters into the CTA's shared counters, then (thread 0) into the
 // level's trace row; then the grid barrier; block 0 stamps the time.
-template <int THREADS>
-__device__ __forceinline__ void level_barrier(const Params& p, Smem<THREADS>& sm, unsigned& gen,
+template <int THREADS, int MODE>
+__device__ __forceinline__ void level_barrier(const Params& p, Smem<THREADS, MODE>& sm, unsigned& gen,
                                               uint32_t level, uint32_t (&c)[4], int stamp_slot) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -256,7 +260,8 @@ __device__ __forceinline__ void level_barrier(const Params& p, Smem<THREADS>& sm
 template <int MODE, int PULL, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
     constexpr int WPC = THREADS / 32;
-    __shared__ Smem<THREADS> sm;
+    __shared__ Smem<THREADS, MODE> sm;
+    extern __shared__ uint32_t hub[];  // lazy: V_curr bits of the hub prefix [0, 32*hub_words)
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
@@ -283,6 +288,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
             p.B2[w] = 0;
         } else {
             V[w] = make_uint2(seed, seed);
+            if (w < p.hub_words) p.hubV[w] = seed;
         }
     }
     {
@@ -343,6 +349,16 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
         }
 
         // ---- pull over the queue (pull_vss, R:src/bfs_engine.cpp:131-146) ----
+        // Dense lazy levels: stage the frozen V_curr bits of the hub prefix in shared memory,
+        // so the visited test of the (mostly hub-bound) hits is served on-chip.
+        const bool hubs = (MODE == 1) && p.hub_words && len >= p.dense_min;
+        const uint32_t hub_n = hubs ? 32u * p.hub_words : 0u;
+        if (hubs) {
+            const uint4* src4 = reinterpret_cast<const uint4*>(p.hubV);
+            uint4* dst4 = reinterpret_cast<uint4*>(hub);
+            for (uint32_t i = threadIdx.x; i < p.hub_words / 4; i += THREADS) dst4[i] = src4[i];
+            __syncthreads();
+        }
         if (gw < NW) {
             for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
                 unsigned long long e = kNoEntry;
@@ -384,10 +400,15 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                         // was visited before this level or is already marked this level.
                         uint2 vw[4];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) vw[c] = cnt[c] ? V[u[c] >> 5] : make_uint2(~0u, ~0u);
+                        for (int c = 0; c < 4; ++c) {
+                            bool need = cnt[c] != 0;
+                            if (need && u[c] < hub_n) need = !((hub[u[c] >> 5] >> (u[c] & 31)) & 1u);
+                            vw[c] = (need && !(p.xflags & 1)) ? V[u[c] >> 5]
+                                                               : make_uint2(need ? 0u : ~0u, need ? 0u : ~0u);
+                        }
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            if (!(((vw[c].x | vw[c].y) >> (u[c] & 31)) & 1u)) {
+                            if (!(((vw[c].x | vw[c].y) >> (u[c] & 31)) & 1u) && !(p.xflags & 2)) {
                                 red_or(&V[u[c] >> 5].y, 1u << (u[c] & 31));
                                 ++ctr[2];
                             }
@@ -422,7 +443,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
         }
 
         if (MODE == 1) {
-            level_barrier<THREADS>(p, sm, gen, level, ctr, 1);
+            level_barrier(p, sm, gen, level, ctr, 1);
             // ---- stage 2 (R:src/bfs_engine.cpp:296-338): chunked word sweep ----
             uint32_t* Fd = p.B2;  // this level's diff words (the reference's F_curr, :310-311)
             const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
@@ -437,7 +458,10 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                     const uint2 v = V[w];
                     diff = v.y & ~v.x;
                     Fd[w] = diff;
-                    if (diff) V[w].x = v.y;
+                    if (diff) {
+                        V[w].x = v.y;
+                        if (w < p.hub_words) p.hubV[w] = v.y;
+                    }
                     for (uint32_t d = diff; d; ) {
                         const int bsel = (__ffs(d) - 1) >> 3;
                         d &= ~(0xFFu << (8 * bsel));
@@ -456,7 +480,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                 }
             }
             unsigned long long cta_total = 0;
-            block_excl_scan<THREADS>(sm, mine, &cta_total);
+            block_excl_scan(sm, mine, &cta_total);
             // publish this CTA's count, then sum the predecessors' (level-tagged)
             if (threadIdx.x == 0) {
                 const unsigned long long tag = ((unsigned long long)level << 40) | cta_total;
@@ -496,7 +520,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                     }
                 }
                 unsigned long long it_total = 0;
-                unsigned long long pos = running + block_excl_scan<THREADS>(sm, cnt, &it_total);
+                unsigned long long pos = running + block_excl_scan(sm, cnt, &it_total);
 #pragma unroll
                 for (int bsel = 0; bsel < 4; ++bsel) {
                     const unsigned long long aux = (unsigned long long)((diff >> (8 * bsel)) & 0xFFu) << 32;
@@ -513,7 +537,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                 ctr[1] += 1;
             }
         }
-        level_barrier<THREADS>(p, sm, gen, level, ctr, 2);
+        level_barrier(p, sm, gen, level, ctr, 2);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
 }
@@ -543,6 +567,10 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     bar_.alloc(2);
     trace_.alloc(8ull * trace_cap_);
     tstamp_.alloc(3ull * trace_cap_);
+    // hub prefix staged in shared memory on dense lazy levels: at most what one SM's
+    // shared memory holds (a multiple of 4 words for 16-byte staging copies)
+    hub_words_max_ = (uint32_t)std::min<uint64_t>((words_ + 3) / 4 * 4, 56u * 1024);
+    hubV_.alloc(hub_words_max_ ? hub_words_max_ : 4);
     CK(cudaMallocHost(&pinned_, 8 * sizeof(unsigned long long)));
 }
 
@@ -561,6 +589,30 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
     if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
+    // Lazy: give each co-resident CTA an equal share of the SM's shared memory for the
+    // hub prefix (minus the static part), rounded down to 16-byte granules.
+    uint32_t hub_words = 0;
+    size_t dyn = 0;
+    if (opt.mode == Mode::Lazy && !opt.no_hub_cache) {
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, kern));
+        int dev = 0, smem_sm = 0, smem_blk = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+        CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const int64_t share = std::min<int64_t>(smem_sm / per_sm - 1024, smem_blk) - (int64_t)fa.sharedSizeBytes;
+        if (share >= 1024) {
+            hub_words = (uint32_t)std::min<uint64_t>(hub_words_max_, (uint64_t)share / 4 / 4 * 4);
+            dyn = (size_t)hub_words * 4;
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+            int check = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&check, kern, threads, dyn));
+            if (check < per_sm) {  // keep the register-limited occupancy
+                hub_words = 0;
+                dyn = 0;
+            }
+        }
+    }
     uint32_t ctas = (uint32_t)per_sm * (uint32_t)num_sms();
     if (opt.grid_ctas && opt.grid_ctas < ctas) ctas = opt.grid_ctas;
     if (ctas > agg_.count) ctas = (uint32_t)agg_.count;
@@ -588,10 +640,15 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
+    p.hubV = hubV_.p;
+    p.hub_words = hub_words;
+    p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
+    if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);
     cudaStream_t st = stream();
     CK(cudaMemsetAsync(bar_.p, 0, 2 * sizeof(unsigned), st));
     void* args[] = {&p};
-    CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, 0, st));
+    CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, dyn, st));
+    last_hub_words_ = hub_words;
     g_launches.fetch_add(1);
     last_ctas_ = ctas;
     last_threads_ = threads;

@@ -282,6 +282,20 @@ int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint3
     API_END
 }
 
+int blest_order_degree(blest_graph g, uint32_t* forward, int host) {
+    API_BEGIN
+    NEED(g && (forward || g->g.n == 0), "null argument");
+    const uint32_t n = g->g.n;
+    if (host) {
+        DevBuf<uint32_t> f(n ? n : 1);
+        degree_order_permutation(g->g, f.p);
+        if (n) CK(cudaMemcpy(forward, f.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    } else {
+        degree_order_permutation(g->g, forward);
+    }
+    API_END
+}
+
 int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward) {
     API_BEGIN
     NEED(forward || n == 0, "null argument");

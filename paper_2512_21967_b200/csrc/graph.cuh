@@ -44,6 +44,9 @@ DeviceGraph graph_transpose(const DeviceGraph& g);
 // Seeded relabel permutation: forward[i] = rank of (hash64(seed, i), i).
 void relabel_permutation(uint32_t n, uint64_t seed, uint32_t* forward_dev);
 
+// Hub-first pre-pass: forward[u] = rank of (out-degree desc, id asc).
+void degree_order_permutation(const DeviceGraph& g, uint32_t* forward_dev);
+
 // Out-degree array (uint32, n entries) on device.
 void graph_out_degrees(const DeviceGraph& g, uint32_t* deg_dev);
 
