@@ -111,7 +111,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def prepare(config: str, ordering_override: str | None, window: int, prepass: str = "none"):
+def prepare(config: str, ordering_override: str | None, window: int, prepass: str = "none",
+            postpass: str = "none"):
     """Generate -> (relabel) -> plan/order -> permute -> build, all on the GPU."""
     import paper_2512_21967_b200 as B
     kind, prm, ordering, desc = CONFIGS[config]
@@ -133,6 +134,8 @@ def prepare(config: str, ordering_override: str | None, window: int, prepass: st
     pre = B.PrePass.DegreeSort if prepass == "degree" else B.PrePass.None_
     plan = B.select_plan(g, 8, B.SelectDefaults(window_size=window, force=force, pre_pass=pre))
     perm = B.make_permutation(g, plan, 8, seed=7)
+    if postpass == "hub-blocks":
+        perm = B.api.hub_blocks(g, perm)
     t_order = time.time() - t0
     t0 = time.time()
     gp = g if perm.is_identity() else B.apply_permutation(g, perm)
@@ -191,6 +194,7 @@ def main():
     ap.add_argument("--order", default=None, choices=["auto", "identity", "rcm", "jaccard", "random"])
     ap.add_argument("--window", type=int, default=1 << 16)
     ap.add_argument("--prepass", default="none", choices=["none", "degree"])
+    ap.add_argument("--postpass", default="none", choices=["none", "hub-blocks"])
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (256/512/1024; 0 = default)")
     ap.add_argument("--source-seed", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
@@ -220,7 +224,7 @@ def main():
     stream = torch.cuda.current_stream()
     L.check(lib.blest_set_stream(C.c_void_p(stream.cuda_stream)))
 
-    prep = prepare(args.config, args.order, args.window, args.prepass)
+    prep = prepare(args.config, args.order, args.window, args.prepass, args.postpass)
     g, b, plan, perm = prep["g"], prep["b"], prep["plan"], prep["perm"]
     cfg = B.EngineConfig(mode=B.engine_mode_from_string(args.mode), pull=args.pull)
     mode = B.choose_mode(b, plan, cfg)
@@ -234,7 +238,7 @@ def main():
     threads = os.cpu_count() or 1
     workload = dict(workload=args.config, graph=prep["desc"], n=n, arcs=int(b.m),
                     num_vss=int(b.num_vss), ordering=plan.strategy.value, engine=mode.value,
-                    pull=args.pull, prepass=args.prepass, sources=len(mine) * world, source_seed=args.source_seed,
+                    pull=args.pull, prepass=args.prepass, postpass=args.postpass, sources=len(mine) * world, source_seed=args.source_seed,
                     l2="inputs larger than L2 (BVSS %.2f GB > 126 MB), no flush" % (b.num_vss * 644 / 1e9),
                     prep_s=prep["times"], parallelism=f"source-sharded x{world}" if world > 1 else "1 GPU")
 

@@ -98,6 +98,10 @@ int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint3
 /* Hub-first pre-pass (new; composable like R:include/blest/ordering.hpp PrePass):
  * forward[u] = rank of (out-degree descending, id ascending). */
 int blest_order_degree(blest_graph g, uint32_t* forward, int host);
+/* Hub-block post-pass (new): after `base_forward` (host, may be NULL = identity), order the
+ * 8-id slice-set blocks by descending degree sum, keeping each block intact (slice sets,
+ * compression and VSS dequeues unchanged). Writes the composed forward map (host). */
+int blest_order_hub_blocks(blest_graph g, const uint32_t* base_forward, uint32_t* forward);
 /* random_order(n, seed) (R:include/blest/ordering.hpp:58, R:src/ordering.cpp:268-275). */
 int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward);
 /* Harness relabel: forward[i] = rank of (splitmix64(seed, i), i); host or device output. */

@@ -101,6 +101,7 @@ SIGNATURES = {
     "blest_order_jaccard_windows": (i32, [vp, u32, u32, vp]),
     "blest_order_random": (i32, [u32, u64, vp]),
     "blest_order_degree": (i32, [vp, vp, i32]),
+    "blest_order_hub_blocks": (i32, [vp, vp, vp]),
     "blest_relabel_permutation": (i32, [u32, u64, vp, i32]),
     "blest_pick_sources": (i32, [vp, u32, u64, i32, vp]),
     "blest_bvss_build": (i32, [vp, P(vp)]),

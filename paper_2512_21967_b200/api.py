@@ -327,6 +327,15 @@ def make_permutation(g: Graph, plan: OrderingPlan, sigma: int = 8, seed: int = 0
     return jaccard_with_windows(g, sigma, plan.window_size)
 
 
+def hub_blocks(g: Graph, base: Permutation | None = None) -> Permutation:
+    """Hub-block post-pass (B200 addition): 8-id slice-set blocks sorted by descending
+    degree sum after `base`; slice sets, compression and dequeues are unchanged."""
+    f = np.zeros(max(g.num_vertices(), 1), np.uint32)
+    bf = base.forward_map() if base is not None else None
+    L.check(L.lib().blest_order_hub_blocks(g.handle, _ptr(bf) if bf is not None else None, _ptr(f)))
+    return Permutation(f[: g.num_vertices()])
+
+
 def degree_order(g: Graph) -> Permutation:
     """Hub-first pre-pass: rank by (out-degree descending, id ascending), on the GPU."""
     f = np.zeros(max(g.num_vertices(), 1), np.uint32)

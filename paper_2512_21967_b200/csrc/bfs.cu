@@ -50,8 +50,8 @@ struct Params {
     const uint32_t* __restrict__ masks;
     const uint4* __restrict__ rows4;
     uint32_t* L;
-    uint32_t* B0;  // eager F0 | lazy V (uint2 {cur, next}, spans B0..B1)
-    uint32_t* B1;  // eager F1
+    uint32_t* B0;  // eager F0 | lazy V_curr
+    uint32_t* B1;  // eager F1 | lazy V_next
     uint32_t* B2;  // eager F2 | lazy per-level diff
     unsigned long long* Q0;
     unsigned long long* Q1;
@@ -65,8 +65,8 @@ struct Params {
     uint32_t src;
     uint32_t cap;
     uint32_t num_warps;
-    uint32_t* hubV;          // lazy: copy of V_curr words [0, hub_words) (the hub prefix)
-    uint32_t hub_words;      // words staged in shared memory on dense levels (0 = off)
+    uint32_t hub_words;      // lazy: V_curr words [0, hub_words) staged in shared memory on
+                             // dense levels (0 = off; the L1 then caches the hub prefix)
     uint64_t dense_min;      // queue length from which a level stages the hub prefix
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
 };
@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
     unsigned gen = 0;
     const uint64_t pol = evict_first_policy();
     if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
-    uint2* V = reinterpret_cast<uint2*>(p.B0);  // lazy {cur, next}
+    uint32_t* Vc = p.B0;  // lazy V_curr: frozen during stage 1 (L1-cacheable)
+    uint32_t* Vn = p.B1;  // lazy V_next: REDs at L2, read with L1-bypassing loads
 
     // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
     const uint32_t src = p.src;
@@ -287,8 +288,8 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
             p.B1[w] = seed;  // F[1] = F_curr of level 1
             p.B2[w] = 0;
         } else {
-            V[w] = make_uint2(seed, seed);
-            if (w < p.hub_words) p.hubV[w] = seed;
+            Vc[w] = seed;
+            Vn[w] = seed;
         }
     }
     {
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
         const bool hubs = (MODE == 1) && p.hub_words && len >= p.dense_min;
         const uint32_t hub_n = hubs ? 32u * p.hub_words : 0u;
         if (hubs) {
-            const uint4* src4 = reinterpret_cast<const uint4*>(p.hubV);
+            const uint4* src4 = reinterpret_cast<const uint4*>(Vc);
             uint4* dst4 = reinterpret_cast<uint4*>(hub);
             for (uint32_t i = threadIdx.x; i < p.hub_words / 4; i += THREADS) dst4[i] = src4[i];
             __syncthreads();
@@ -398,18 +399,22 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                     if (MODE == 1) {
                         // stage-1 sink (:286-289): relaxed OR into V_next unless the vertex
                         // was visited before this level or is already marked this level.
-                        uint2 vw[4];
+                        // visited before this level? (V_curr; hub prefix from shared memory)
+                        uint32_t vw[4];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             bool need = cnt[c] != 0;
                             if (need && u[c] < hub_n) need = !((hub[u[c] >> 5] >> (u[c] & 31)) & 1u);
-                            vw[c] = (need && !(p.xflags & 1)) ? V[u[c] >> 5]
-                                                               : make_uint2(need ? 0u : ~0u, need ? 0u : ~0u);
+                            vw[c] = (need && !(p.xflags & 1)) ? Vc[u[c] >> 5] : (need ? 0u : ~0u);
                         }
+                        // not yet: already marked this level by anyone? (V_next at L2)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (!((vw[c] >> (u[c] & 31)) & 1u) && !(p.xflags & 2)) vw[c] = ld_relaxed_gpu(Vn + (u[c] >> 5));
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            if (!(((vw[c].x | vw[c].y) >> (u[c] & 31)) & 1u) && !(p.xflags & 2)) {
-                                red_or(&V[u[c] >> 5].y, 1u << (u[c] & 31));
+                            if (!((vw[c] >> (u[c] & 31)) & 1u)) {
+                                red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
                                 ++ctr[2];
                             }
                         }
@@ -455,13 +460,10 @@ __global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
                 const uint64_t w = wb + threadIdx.x;
                 uint32_t diff = 0;
                 if (w < w1) {
-                    const uint2 v = V[w];
-                    diff = v.y & ~v.x;
+                    const uint32_t nx = Vn[w];
+                    diff = nx & ~Vc[w];
                     Fd[w] = diff;
-                    if (diff) {
-                        V[w].x = v.y;
-                        if (w < p.hub_words) p.hubV[w] = v.y;
-                    }
+                    if (diff) Vc[w] = nx;
                     for (uint32_t d = diff; d; ) {
                         const int bsel = (__ffs(d) - 1) >> 3;
                         d &= ~(0xFFu << (8 * bsel));
@@ -567,10 +569,9 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     bar_.alloc(2);
     trace_.alloc(8ull * trace_cap_);
     tstamp_.alloc(3ull * trace_cap_);
-    // hub prefix staged in shared memory on dense lazy levels: at most what one SM's
-    // shared memory holds (a multiple of 4 words for 16-byte staging copies)
-    hub_words_max_ = (uint32_t)std::min<uint64_t>((words_ + 3) / 4 * 4, 56u * 1024);
-    hubV_.alloc(hub_words_max_ ? hub_words_max_ : 4);
+    // hub prefix staged in shared memory on dense lazy levels (opt-in): at most what one
+    // SM's shared memory holds, whole 16-byte granules inside the V_curr array
+    hub_words_max_ = (uint32_t)std::min<uint64_t>(words_ / 4 * 4, 56u * 1024);
     CK(cudaMallocHost(&pinned_, 8 * sizeof(unsigned long long)));
 }
 
@@ -593,7 +594,9 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     // hub prefix (minus the static part), rounded down to 16-byte granules.
     uint32_t hub_words = 0;
     size_t dyn = 0;
-    if (opt.mode == Mode::Lazy && !opt.no_hub_cache) {
+    const char* hub_env = getenv("BLEST_HUB_CACHE");
+    const bool hub_cache = opt.hub_cache || (hub_env && atoi(hub_env) != 0);
+    if (opt.mode == Mode::Lazy && hub_cache && hub_words_max_) {
         cudaFuncAttributes fa;
         CK(cudaFuncGetAttributes(&fa, kern));
         int dev = 0, smem_sm = 0, smem_blk = 0;
@@ -640,7 +643,6 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
-    p.hubV = hubV_.p;
     p.hub_words = hub_words;
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);

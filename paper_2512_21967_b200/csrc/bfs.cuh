@@ -19,7 +19,7 @@ struct EngineOptions {
     uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
-    bool no_hub_cache = false;  // lazy: disable the shared-memory hub-prefix visited cache
+    bool hub_cache = false;  // lazy: stage the hub prefix of V_curr in shared memory
 };
 
 // One row per level, same fields as LevelTrace (R:include/blest/bfs_engine.hpp:27-37).
@@ -67,7 +67,6 @@ private:
     DevBuf<unsigned long long> q_;       // 3 * max(num_vss, 1) entries
     DevBuf<unsigned long long> ctl_;     // qlen[4], result[4]
     DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA counts
-    DevBuf<uint32_t> hubV_;              // lazy: V_curr words of the hub prefix
     uint32_t hub_words_max_ = 0, last_hub_words_ = 0;
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8

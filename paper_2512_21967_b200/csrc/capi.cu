@@ -296,6 +296,20 @@ int blest_order_degree(blest_graph g, uint32_t* forward, int host) {
     API_END
 }
 
+int blest_order_hub_blocks(blest_graph g, const uint32_t* base_forward, uint32_t* forward) {
+    API_BEGIN
+    NEED(g && (forward || g->g.n == 0), "null argument");
+    const uint32_t n = g->g.n;
+    DevBuf<uint32_t> base, f(n ? n : 1);
+    if (base_forward && n) {
+        base.alloc(n);
+        CK(cudaMemcpy(base.p, base_forward, (size_t)n * 4, cudaMemcpyHostToDevice));
+    }
+    hub_block_permutation(g->g, base_forward ? base.p : nullptr, f.p);
+    if (n) CK(cudaMemcpy(forward, f.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    API_END
+}
+
 int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward) {
     API_BEGIN
     NEED(forward || n == 0, "null argument");
