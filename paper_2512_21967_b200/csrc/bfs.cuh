@@ -66,7 +66,9 @@ private:
     DevBuf<uint32_t> bits_;              // 3 * words_
     DevBuf<unsigned long long> q_;       // 3 * max(num_vss, 1) entries
     DevBuf<unsigned long long> ctl_;     // qlen[4], result[4]
-    DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA counts
+    DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA VSS counts
+    DevBuf<unsigned long long> aggS_;    // lazy stage-2 per-CTA slice-set counts
+    DevBuf<unsigned long long> sl_;      // lazy queue: active slice sets
     uint32_t hub_words_max_ = 0, last_hub_words_ = 0;
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
