@@ -89,13 +89,13 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 }
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
     uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
                  : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p, uint64_t pol) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
     return v;
 }
@@ -107,6 +107,13 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned* p) {
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Same load without the compiler barrier: for data whose ordering the caller does not
+// need (e.g. a racy pre-check before an idempotent RED), so loads keep overlapping.
+__device__ __forceinline__ uint32_t ld_l2_u32(const uint32_t* p) {
+    uint32_t v;
+    asm("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
