@@ -10,7 +10,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libblest_b200.so")
+LIB_PATH = os.environ.get("BLEST_LIB") or os.path.join(HERE, "libblest_b200.so")
 
 BLEST_OK, BLEST_EINVAL, BLEST_ERUNTIME, BLEST_ELOGIC, BLEST_ECUDA, BLEST_ENOMEM = 0, -1, -2, -3, -4, -5
 MODE_EAGER, MODE_LAZY, MODE_AUTO = 0, 1, 2

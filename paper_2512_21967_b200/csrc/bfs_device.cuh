@@ -8,7 +8,10 @@
 namespace blestgpu {
 namespace bfsdev {
 
-constexpr int kBatch = 4;         // VSSs in flight per warp
+#ifndef BLEST_KBATCH
+#define BLEST_KBATCH 4
+#endif
+constexpr int kBatch = BLEST_KBATCH;  // VSSs in flight per warp
 constexpr int kPushCap = 64;      // per-warp push buffer entries (eager)
 constexpr unsigned long long kNoEntry = ~0ull;
 

@@ -103,11 +103,15 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
 
         // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
+            // queue entries of the next batch are fetched while this batch is processed
+            unsigned long long e_next = kNoEntry;
+            if (lane < kBatch && gw + (uint64_t)lane * NW < len) e_next = Qc[gw + (uint64_t)lane * NW];
             for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
-                unsigned long long e = kNoEntry;
+                const unsigned long long e = e_next;
+                e_next = kNoEntry;
                 if (lane < kBatch) {
-                    const uint64_t pos = p0 + (uint64_t)lane * NW;
-                    if (pos < len) e = Qc[pos];
+                    const uint64_t pos = p0 + (uint64_t)NW * kBatch + (uint64_t)lane * NW;
+                    if (pos < len) e_next = Qc[pos];
                 }
                 uint32_t mk[kBatch];
                 uint4 rw[kBatch];
@@ -190,23 +194,18 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
             const unsigned long long tag = ((unsigned long long)level << 40) | cta_vss;
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag) : "memory");
         }
-        if (warp == 0) {
-            unsigned long long before = 0;
-            for (uint32_t c = lane; c < blockIdx.x; c += 32) {
-                unsigned long long x;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
-                } while ((x >> 40) != level);
-                before += x & kTagMask;
-            }
-            before = warp_sum(before);
-            if (lane == 0) {
-                sm.base = before;
-                if (blockIdx.x == gridDim.x - 1) p.ctl[0] = before + cta_vss;  // next level's length
-            }
+        // sum the predecessors' counts with every thread (one or two rounds of loads)
+        unsigned long long before = 0;
+        for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
+            unsigned long long x;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
+            } while ((x >> 40) != level);
+            before += x & kTagMask;
         }
-        __syncthreads();
-        unsigned long long running = sm.base;
+        unsigned long long running = 0;
+        block_excl_scan(sm, before, &running);
+        if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) p.ctl[0] = running + cta_vss;  // next length
         if (threadIdx.x == 0) ctr[3] += (uint32_t)cta_vss;
         // pass B: expand the chunk's sets into the queue, slice-set order; warp-cooperative
         for (uint64_t wb = w0; wb < w1; wb += THREADS) {
