@@ -30,6 +30,7 @@
 // order — with no contended queue-tail atomic at all.
 #include <algorithm>
 #include <atomic>
+#include <string>
 
 #include "bfs.cuh"
 #include "bfs_device.cuh"
@@ -38,7 +39,9 @@ namespace blestgpu {
 
 extern std::atomic<uint64_t> g_launches;
 
-void* lazy_kernel(int pull, int threads);  // bfs_lazy.cu
+void* lazy_kernel(int pull, int threads);        // bfs_lazy.cu (register-pipelined variant)
+void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
+size_t lazy_tma_smem();
 
 namespace {
 using namespace bfsdev;
@@ -369,22 +372,31 @@ BfsEngine::~BfsEngine() {
 
 void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (src >= b_.n) throw InvalidArgument("bfs source out of range");
-    const int threads = opt.threads ? (int)opt.threads : 512;
+    const char* var_env = getenv("BLEST_LAZY_VARIANT");
+    const bool lazy_tma = opt.mode == Mode::Lazy && !(opt.lazy_plain || (var_env && std::string(var_env) == "plain"));
+    const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
+    const int consumers = nc_env ? atoi(nc_env) : 16;
+    const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
         kern = opt.pull == Pull::Mma ? pick_kernel<0, 1>(threads) : pick_kernel<0, 0>(threads);
     else
-        kern = lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
+        kern = lazy_tma ? lazy_tma_kernel(opt.pull == Pull::Mma ? 1 : 0, consumers)
+                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
+    size_t dyn = 0;
+    if (lazy_tma) {
+        dyn = lazy_tma_smem();
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    }
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dyn));
     if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
     // Lazy: give each co-resident CTA an equal share of the SM's shared memory for the
     // hub prefix (minus the static part), rounded down to 16-byte granules.
     uint32_t hub_words = 0;
-    size_t dyn = 0;
     const char* hub_env = getenv("BLEST_HUB_CACHE");
     const bool hub_cache = opt.hub_cache || (hub_env && atoi(hub_env) != 0);
-    if (opt.mode == Mode::Lazy && hub_cache && hub_words_max_) {
+    if (opt.mode == Mode::Lazy && !lazy_tma && hub_cache && hub_words_max_) {
         cudaFuncAttributes fa;
         CK(cudaFuncGetAttributes(&fa, kern));
         int dev = 0, smem_sm = 0, smem_blk = 0;

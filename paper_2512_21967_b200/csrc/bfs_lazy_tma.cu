@@ -1,0 +1,388 @@
+// Lazy engine (BLEST Alg. 3; run_lazy, R:src/bfs_engine.cpp:238-350), TMA-pipelined:
+// one fused persistent cooperative kernel per source.
+//
+// Queue. The level's queue is the ascending list SL of active slice sets, each entry the
+// set id and the queue position of its first VSS; positions in between are implicit
+// (v = real_ptrs[s] + offset). The dequeued VSS multiset — hence every counter — is the
+// reference's (:323-330 pushes each set's whole VSS range), but stage 2 writes one entry
+// per set, so it is balanced even when a hub set owns thousands of VSSs.
+//
+// Stage 1 (pull, :273-292), warp-specialised per CTA:
+//   producer warp  — owns the CTA's contiguous queue positions [c·T/G, (c+1)·T/G), walks
+//                    SL with a 32-set window in its lanes, and for every stage of kSB
+//                    positions issues cp.async.bulk copies of each VSS's 128 B mask line
+//                    and 512 B row-id block into a shared-memory ring slot, completing on
+//                    that slot's mbarrier (expect_tx); α of each VSS rides in a slot header;
+//   consumer warps — take ring slots round-robin, copy the slot to registers, release it,
+//                    AND each lane's masks with α and run the visited test per nonzero
+//                    column: V_curr (frozen during the stage, L1-cached), then V_next at L2,
+//                    then a fire-and-forget RED (legal per SURVEY §8(a) pitfall 7).
+// The HBM stream thus runs kNS stages ahead of the latency-bound visited checks instead of
+// waiting behind them.
+//
+// Stage 2 (word sweep, :296-338): each CTA owns a contiguous chunk of the ⌈n/32⌉ words.
+// Pass A: diff = V_next & ~V_curr, V_curr |= diff, diff words kept (they carry α for the
+// next level, like the reference's in-place F_curr :310-311), levels written with one
+// coalesced 128 B store per changed word, set/VSS counts reduced. The CTA publishes both
+// counts (tagged with the level) and sums its predecessors'; pass B writes its SL entries.
+#include "bfs.cuh"
+#include "bfs_device.cuh"
+
+namespace blestgpu {
+
+namespace {
+using namespace bfsdev;
+
+constexpr unsigned long long kTagMask = (1ull << 40) - 1;
+constexpr int kSB = 4;                         // VSSs per ring slot
+constexpr int kNS = 24;                        // ring slots per CTA
+constexpr uint32_t kSlotBytes = kSB * 640;     // 4 x (128 B masks + 512 B row ids)
+
+struct SlotHdr {
+    uint32_t count;
+    uint32_t alpha;  // 4 frontier bytes
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+
+// One warp's view of 32 consecutive SL entries.
+struct SetWindow {
+    uint32_t base;   // SL index held by lane 0
+    uint64_t first;  // lane's first queue position (UINT64_MAX past the list)
+    uint32_t b;      // lane's first VSS id (real_ptrs[s])
+    uint32_t alpha;  // lane's frontier byte
+    uint64_t wend;   // one past the last position covered by the window
+};
+
+__device__ __forceinline__ void load_window(const Params& p, const uint8_t* Fd8, uint32_t base, uint32_t S,
+                                            uint64_t T, SetWindow& w) {
+    const unsigned lane = lane_id();
+    const uint32_t k = base + lane;
+    uint64_t first = ~0ull, nxt = T;
+    uint32_t b = 0, alpha = 0;
+    if (k < S) {
+        const unsigned long long e = p.SL[k];
+        first = e >> 32;
+        const uint32_t ss = (uint32_t)e;
+        b = p.rp[ss];
+        alpha = Fd8[ss];
+        if (lane == 31 && k + 1 < S) nxt = p.SL[k + 1] >> 32;
+    }
+    w.base = base;
+    w.first = first;
+    w.b = b;
+    w.alpha = alpha;
+    w.wend = (base + 32 < S) ? __shfl_sync(0xffffffffu, nxt, 31) : T;
+}
+
+// Largest SL index k with first(k) <= pos (first(0) = 0, entries ascending).
+__device__ __forceinline__ uint32_t find_set(const Params& p, uint32_t S, uint64_t pos) {
+    const unsigned lane = lane_id();
+    uint32_t lo = 0, hi = S;
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t idx = lo + lane * step;
+        const bool ok = idx < hi && (p.SL[idx] >> 32) <= pos;
+        const unsigned ball = __ballot_sync(0xffffffffu, ok);
+        lo = lo + (31 - __clz(ball)) * step;
+        hi = min(hi, lo + step);
+    }
+    const uint32_t idx = lo + lane;
+    const bool ok = idx < hi && (p.SL[idx] >> 32) <= pos;
+    return lo + (31 - __clz(__ballot_sync(0xffffffffu, ok)));
+}
+
+template <int PULL, int NC>
+__global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
+    constexpr int THREADS = 32 * (NC + 1);
+    __shared__ Smem<THREADS, 1> sm;
+    __shared__ __align__(8) uint64_t full[kNS], empty[kNS];
+    __shared__ SlotHdr hdr[kNS];
+    extern __shared__ __align__(128) uint8_t ring[];  // kNS slots of kSlotBytes
+    const unsigned lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    const uint64_t gthreads = (uint64_t)gridDim.x * THREADS;
+    unsigned gen = 0;
+    const uint64_t pol = evict_first_policy();
+    uint32_t* Vc = p.B0;
+    uint32_t* Vn = p.B1;
+    uint32_t* Fd = p.B2;
+    const uint8_t* Fd8 = reinterpret_cast<const uint8_t*>(Fd);
+    if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kNS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
+    const uint32_t src = p.src;
+    const uint32_t sset = src / kSigma;
+    const uint32_t seed_b = p.rp[sset], seed_e = p.rp[sset + 1];
+    for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
+    const uint32_t src_word = src >> 5, src_bit = 1u << (src & 31);
+    for (uint64_t w = gtid; w < p.words; w += gthreads) {
+        const uint32_t seed = (w == src_word) ? src_bit : 0u;
+        Vc[w] = seed;
+        Vn[w] = seed;
+        Fd[w] = seed;  // α of the source's set for level 1
+    }
+    if (threadIdx.x == 0) {
+        p.agg[blockIdx.x] = 0;
+        p.aggS[blockIdx.x] = 0;
+    }
+    if (gtid == 0) {
+        p.SL[0] = sset;                        // first position 0
+        p.ctl[0] = seed_e - seed_b;            // T: VSSs queued for the level
+        p.ctl[1] = (seed_e > seed_b) ? 1 : 0;  // S: slice sets queued
+        for (int i = 2; i < 8; ++i) p.ctl[i] = 0;
+        for (int i = 0; i < 8; ++i) p.trace[i] = 0;
+    }
+    grid_barrier(p.bar, gen);
+
+    uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
+    uint32_t ring_base = 0;           // slots consumed by earlier levels (same in every warp)
+    uint32_t level = 1;
+    for (;; ++level) {
+        const unsigned long long T = ld_relaxed_gpu_u64(&p.ctl[0]);
+        const uint32_t S = (uint32_t)ld_relaxed_gpu_u64(&p.ctl[1]);
+        if (T == 0) break;
+        if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
+            if (gtid == 0) p.ctl[6] = 1;
+            break;
+        }
+        if (gtid == 0) {
+            if (level - 1 < p.trace_cap) {
+                p.trace[8ull * (level - 1) + 0] = level;
+                p.trace[8ull * (level - 1) + 1] = T;
+                p.tstamp[3ull * (level - 1)] = globaltimer();
+            } else {
+                atomicAdd(&p.trace[8ull * (p.trace_cap - 1) + 1], T);
+            }
+            if (level < p.trace_cap)
+                for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
+        }
+
+        // ---- stage 1 ----
+        const uint64_t lo = (uint64_t)blockIdx.x * T / gridDim.x;
+        const uint64_t hi = (uint64_t)(blockIdx.x + 1) * T / gridDim.x;
+        const uint32_t nst = (uint32_t)((hi - lo + kSB - 1) / kSB);
+        if (warp == 0) {
+            // producer
+            if (nst) {
+                SetWindow win;
+                load_window(p, Fd8, find_set(p, S, lo), S, T, win);
+                for (uint32_t i = 0; i < nst; ++i) {
+                    const uint32_t g = ring_base + i, s = g % kNS;
+                    const uint64_t sp = lo + (uint64_t)i * kSB;
+                    const uint32_t cnt = (hi - sp < (uint64_t)kSB) ? (uint32_t)(hi - sp) : (uint32_t)kSB;
+                    if (sp + cnt - 1 >= win.wend) {  // slide the window to the set holding sp
+                        const unsigned own = __ballot_sync(0xffffffffu, win.first <= sp);
+                        const uint32_t nb = (sp >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
+                        load_window(p, Fd8, nb, S, T, win);
+                    }
+                    uint32_t myv = 0, alphas = 0;
+#pragma unroll
+                    for (int j = 0; j < kSB; ++j) {
+                        const uint64_t q = sp + j;
+                        const int l = 31 - __clz(__ballot_sync(0xffffffffu, win.first <= q));
+                        const uint32_t v = __shfl_sync(0xffffffffu, win.b, l) +
+                                           (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
+                        const uint32_t a = __shfl_sync(0xffffffffu, win.alpha, l);
+                        if (lane == (unsigned)j) myv = v;
+                        alphas |= (j < (int)cnt ? a : 0u) << (8 * j);
+                    }
+                    if (g >= kNS) mbar_wait(&empty[s], ((g / kNS) - 1) & 1);
+                    if (lane == 0) {
+                        hdr[s].count = cnt;
+                        hdr[s].alpha = alphas;
+                        mbar_arrive_expect_tx(&full[s], cnt * 640);
+                    }
+                    __syncwarp();
+                    if (lane < cnt) {
+                        uint8_t* slot = ring + (size_t)s * kSlotBytes;
+                        bulk_g2s(slot + lane * 128, p.masks + 32ull * myv, 128, &full[s], pol);
+                        bulk_g2s(slot + kSB * 128 + lane * 512, p.rows4 + 32ull * myv, 512, &full[s], pol);
+                    }
+                }
+            }
+        } else {
+            // consumers
+            for (uint32_t i = warp - 1; i < nst; i += NC) {
+                const uint32_t g = ring_base + i, s = g % kNS;
+                mbar_wait(&full[s], (g / kNS) & 1);
+                const uint32_t cnt = hdr[s].count, alphas = hdr[s].alpha;
+                const uint8_t* slot = ring + (size_t)s * kSlotBytes;
+                uint32_t mk[kSB];
+                uint4 rw[kSB];
+#pragma unroll
+                for (int j = 0; j < kSB; ++j) {
+                    mk[j] = reinterpret_cast<const uint32_t*>(slot + j * 128)[lane];
+                    rw[j] = reinterpret_cast<const uint4*>(slot + kSB * 128 + j * 512)[lane];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+                for (int j = 0; j < kSB; ++j) {
+                    if (j >= (int)cnt) break;  // warp-uniform
+                    uint32_t c4[4];
+                    column_counts<PULL>(mk[j], (alphas >> (8 * j)) & 0xFFu, c4);
+                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                    uint32_t vw[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) vw[c] = c4[c] ? Vc[u[c] >> 5] : ~0u;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (!((vw[c] >> (u[c] & 31)) & 1u)) vw[c] = ld_l2_u32(Vn + (u[c] >> 5));
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (!((vw[c] >> (u[c] & 31)) & 1u)) {
+                            red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
+                            ++ctr[2];
+                        }
+                    }
+                }
+            }
+        }
+        ring_base += nst;
+        level_barrier(p, sm, gen, level, ctr, 1);
+
+        // ---- stage 2: chunked word sweep ----
+        const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
+        const uint64_t w0 = (uint64_t)blockIdx.x * per;
+        const uint64_t w1 = min(w0 + per, p.words);
+        unsigned long long my_vss = 0, my_sets = 0;
+        // pass A
+        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
+            const uint64_t w = wb + threadIdx.x;
+            uint32_t diff = 0;
+            if (w < w1) {
+                const uint32_t nx = Vn[w];
+                diff = nx & ~Vc[w];
+                Fd[w] = diff;
+                if (diff) Vc[w] = nx;
+                for (uint32_t d = diff; d;) {
+                    const int bsel = (__ffs(d) - 1) >> 3;
+                    d &= ~(0xFFu << (8 * bsel));
+                    const uint64_t ss = 4 * w + bsel;
+                    const uint32_t c = p.rp[ss + 1] - p.rp[ss];
+                    my_vss += c;
+                    my_sets += c != 0;  // sets without VSSs push nothing
+                }
+            }
+            ctr[0] += __popc(diff);
+            const uint64_t wwarp = wb + 32 * warp;
+            unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
+            while (ball) {
+                const int k = __ffs(ball) - 1;
+                ball &= ball - 1;
+                const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
+                if ((dk >> lane) & 1u) p.L[32 * (wwarp + k) + lane] = level;
+            }
+        }
+        unsigned long long cta_vss = 0, cta_sets = 0;
+        block_excl_scan(sm, my_vss, &cta_vss);
+        block_excl_scan(sm, my_sets, &cta_sets);
+        if (threadIdx.x == 0) {
+            const unsigned long long tag = (unsigned long long)level << 40;
+            p.aggS[blockIdx.x] = tag | cta_sets;
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag | cta_vss)
+                         : "memory");
+        }
+        unsigned long long bv = 0, bs = 0;
+        for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
+            unsigned long long x;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
+            } while ((x >> 40) != level);
+            bv += x & kTagMask;
+            bs += ld_relaxed_gpu_u64(p.aggS + c) & kTagMask;
+        }
+        unsigned long long run_vss = 0, run_sets = 0;
+        block_excl_scan(sm, bv, &run_vss);
+        block_excl_scan(sm, bs, &run_sets);
+        if (threadIdx.x == 0) {
+            ctr[3] += (uint32_t)cta_vss;
+            if (blockIdx.x == gridDim.x - 1) {  // grid totals: the next level's T, S
+                p.ctl[0] = run_vss + cta_vss;
+                p.ctl[1] = run_sets + cta_sets;
+            }
+        }
+        // pass B: SL entries of the chunk's active sets, ascending
+        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
+            const uint64_t w = wb + threadIdx.x;
+            const uint32_t diff = (w < w1) ? Fd[w] : 0u;
+            unsigned long long nv = 0, ns = 0;
+            uint32_t cnts[4];
+#pragma unroll
+            for (int bsel = 0; bsel < 4; ++bsel) {
+                cnts[bsel] = 0;
+                if ((diff >> (8 * bsel)) & 0xFFu) {
+                    const uint64_t ss = 4 * w + bsel;
+                    cnts[bsel] = p.rp[ss + 1] - p.rp[ss];
+                    nv += cnts[bsel];
+                    ns += cnts[bsel] != 0;
+                }
+            }
+            unsigned long long it_v = 0, it_s = 0;
+            unsigned long long pv = run_vss + block_excl_scan(sm, nv, &it_v);
+            unsigned long long ps = run_sets + block_excl_scan(sm, ns, &it_s);
+#pragma unroll
+            for (int bsel = 0; bsel < 4; ++bsel) {
+                if (cnts[bsel]) {
+                    p.SL[ps++] = (pv << 32) | (4 * w + bsel);
+                    pv += cnts[bsel];
+                }
+            }
+            run_vss += it_v;
+            run_sets += it_s;
+        }
+        level_barrier(p, sm, gen, level, ctr, 2);
+    }
+    if (gtid == 0) p.ctl[4] = level - 1;
+}
+
+}  // namespace
+
+size_t lazy_tma_smem() { return (size_t)kNS * kSlotBytes; }
+
+void* lazy_tma_kernel(int pull, int consumers) {
+    if (consumers == 8) return pull == 1 ? (void*)k_bfs_lazy_tma<1, 8> : (void*)k_bfs_lazy_tma<0, 8>;
+    if (consumers == 16) return pull == 1 ? (void*)k_bfs_lazy_tma<1, 16> : (void*)k_bfs_lazy_tma<0, 16>;
+    throw InvalidArgument("consumer warps per CTA must be 8 or 16");
+}
+
+}  // namespace blestgpu
