@@ -34,13 +34,14 @@ namespace {
 using namespace bfsdev;
 
 constexpr unsigned long long kTagMask = (1ull << 40) - 1;
-constexpr int kSB = 4;                         // VSSs per ring slot
-constexpr int kNS = 24;                        // ring slots per CTA
-constexpr uint32_t kSlotBytes = kSB * 640;     // 4 x (128 B masks + 512 B row ids)
+constexpr int kSB = 16;                        // VSSs per ring slot
+constexpr int kNS = 6;                         // ring slots per CTA
+constexpr int kCB = 4;                         // VSSs a consumer holds in registers at once
+constexpr uint32_t kSlotBytes = kSB * 640;     // 16 x (128 B masks + 512 B row ids)
 
 struct SlotHdr {
     uint32_t count;
-    uint32_t alpha;  // 4 frontier bytes
+    uint32_t alpha[kSB / 4];  // frontier bytes, 4 per word
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -214,28 +215,36 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
                         const uint32_t nb = (sp >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
                         load_window(p, Fd8, nb, S, T, win);
                     }
-                    uint32_t myv = 0, alphas = 0;
+                    // lane j < kSB resolves position sp + j: binary search of the
+                    // window's first positions (5 shuffle steps, all lanes at once)
+                    const uint64_t q = sp + (lane < kSB ? lane : 0);
+                    int l = 0;
 #pragma unroll
-                    for (int j = 0; j < kSB; ++j) {
-                        const uint64_t q = sp + j;
-                        const int l = 31 - __clz(__ballot_sync(0xffffffffu, win.first <= q));
-                        const uint32_t v = __shfl_sync(0xffffffffu, win.b, l) +
-                                           (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
-                        const uint32_t a = __shfl_sync(0xffffffffu, win.alpha, l);
-                        if (lane == (unsigned)j) myv = v;
-                        alphas |= (j < (int)cnt ? a : 0u) << (8 * j);
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint64_t f = __shfl_sync(0xffffffffu, win.first, l + step);
+                        if (f <= q) l += step;
                     }
+                    const uint32_t myv = __shfl_sync(0xffffffffu, win.b, l) +
+                                         (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
+                    const uint32_t mya = (lane < cnt) ? __shfl_sync(0xffffffffu, win.alpha, l) : 0u;
+                    // runs of consecutive VSS ids become one bulk copy each
+                    const uint32_t prevv = __shfl_up_sync(0xffffffffu, myv, 1);
+                    const bool start = lane < cnt && (lane == 0 || prevv + 1 != myv);
+                    const unsigned starts = __ballot_sync(0xffffffffu, start) | (1u << cnt);
+                    const uint32_t run = start ? (__ffs(starts & ~((2u << lane) - 1)) - 1 - lane) : 0u;
                     if (g >= kNS) mbar_wait(&empty[s], ((g / kNS) - 1) & 1);
-                    if (lane == 0) {
-                        hdr[s].count = cnt;
-                        hdr[s].alpha = alphas;
-                        mbar_arrive_expect_tx(&full[s], cnt * 640);
-                    }
+                    const uint32_t a4 = mya | (__shfl_down_sync(0xffffffffu, mya, 1) << 8) |
+                                        (__shfl_down_sync(0xffffffffu, mya, 2) << 16) |
+                                        (__shfl_down_sync(0xffffffffu, mya, 3) << 24);
+                    if (lane < kSB && (lane & 3) == 0) hdr[s].alpha[lane >> 2] = a4;
+                    if (lane == 0) hdr[s].count = cnt;
                     __syncwarp();
-                    if (lane < cnt) {
+                    if (lane == 0) mbar_arrive_expect_tx(&full[s], cnt * 640);
+                    __syncwarp();
+                    if (start) {
                         uint8_t* slot = ring + (size_t)s * kSlotBytes;
-                        bulk_g2s(slot + lane * 128, p.masks + 32ull * myv, 128, &full[s], pol);
-                        bulk_g2s(slot + kSB * 128 + lane * 512, p.rows4 + 32ull * myv, 512, &full[s], pol);
+                        bulk_g2s(slot + lane * 128, p.masks + 32ull * myv, run * 128, &full[s], pol);
+                        bulk_g2s(slot + kSB * 128 + lane * 512, p.rows4 + 32ull * myv, run * 512, &full[s], pol);
                     }
                 }
             }
@@ -244,34 +253,39 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
             for (uint32_t i = warp - 1; i < nst; i += NC) {
                 const uint32_t g = ring_base + i, s = g % kNS;
                 mbar_wait(&full[s], (g / kNS) & 1);
-                const uint32_t cnt = hdr[s].count, alphas = hdr[s].alpha;
+                const uint32_t cnt = hdr[s].count;
                 const uint8_t* slot = ring + (size_t)s * kSlotBytes;
-                uint32_t mk[kSB];
-                uint4 rw[kSB];
+                for (int j0 = 0; j0 < (int)cnt; j0 += kCB) {
+                    const uint32_t alphas = hdr[s].alpha[j0 >> 2];
+                    uint32_t mk[kCB];
+                    uint4 rw[kCB];
 #pragma unroll
-                for (int j = 0; j < kSB; ++j) {
-                    mk[j] = reinterpret_cast<const uint32_t*>(slot + j * 128)[lane];
-                    rw[j] = reinterpret_cast<const uint4*>(slot + kSB * 128 + j * 512)[lane];
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+                    for (int j = 0; j < kCB; ++j) {
+                        mk[j] = reinterpret_cast<const uint32_t*>(slot + (j0 + j) * 128)[lane];
+                        rw[j] = reinterpret_cast<const uint4*>(slot + kSB * 128 + (j0 + j) * 512)[lane];
+                    }
+                    if (j0 + kCB >= (int)cnt) {  // slot fully copied out: hand it back
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[s]);
+                    }
 #pragma unroll
-                for (int j = 0; j < kSB; ++j) {
-                    if (j >= (int)cnt) break;  // warp-uniform
-                    uint32_t c4[4];
-                    column_counts<PULL>(mk[j], (alphas >> (8 * j)) & 0xFFu, c4);
-                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-                    uint32_t vw[4];
+                    for (int j = 0; j < kCB; ++j) {
+                        if (j0 + j >= (int)cnt) break;  // warp-uniform
+                        uint32_t c4[4];
+                        column_counts<PULL>(mk[j], (alphas >> (8 * j)) & 0xFFu, c4);
+                        const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                        uint32_t vw[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) vw[c] = c4[c] ? Vc[u[c] >> 5] : ~0u;
+                        for (int c = 0; c < 4; ++c) vw[c] = c4[c] ? Vc[u[c] >> 5] : ~0u;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (!((vw[c] >> (u[c] & 31)) & 1u)) vw[c] = ld_l2_u32(Vn + (u[c] >> 5));
+                        for (int c = 0; c < 4; ++c)
+                            if (!((vw[c] >> (u[c] & 31)) & 1u)) vw[c] = ld_l2_u32(Vn + (u[c] >> 5));
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        if (!((vw[c] >> (u[c] & 31)) & 1u)) {
-                            red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
-                            ++ctr[2];
+                        for (int c = 0; c < 4; ++c) {
+                            if (!((vw[c] >> (u[c] & 31)) & 1u)) {
+                                red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
+                                ++ctr[2];
+                            }
                         }
                     }
                 }
