@@ -41,7 +41,7 @@ extern std::atomic<uint64_t> g_launches;
 
 void* lazy_kernel(int pull, int threads);        // bfs_lazy.cu (register-pipelined variant)
 void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
-size_t lazy_tma_smem();
+size_t lazy_tma_smem(int consumers);
 
 namespace {
 using namespace bfsdev;
@@ -375,7 +375,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     const char* var_env = getenv("BLEST_LAZY_VARIANT");
     const bool lazy_tma = opt.mode == Mode::Lazy && !(opt.lazy_plain || (var_env && std::string(var_env) == "plain"));
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
-    const int consumers = nc_env ? atoi(nc_env) : 16;
+    const int consumers = nc_env ? atoi(nc_env) : 8;
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
@@ -385,7 +385,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
                         : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
     size_t dyn = 0;
     if (lazy_tma) {
-        dyn = lazy_tma_smem();
+        dyn = lazy_tma_smem(consumers);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     }
     int per_sm = 0;

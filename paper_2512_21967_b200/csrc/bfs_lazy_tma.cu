@@ -35,7 +35,9 @@ using namespace bfsdev;
 
 constexpr unsigned long long kTagMask = (1ull << 40) - 1;
 constexpr int kSB = 16;                        // VSSs per ring slot
-constexpr int kNS = 6;                         // ring slots per CTA
+// Ring slots per CTA = consumer warps: stage g uses slot g % NC and consumer g % NC, so
+// every slot is only ever refilled for the warp that emptied it (a consumer can never
+// wait on a later phase of a slot before the earlier one was consumed).
 constexpr int kCB = 4;                         // VSSs a consumer holds in registers at once
 constexpr uint32_t kSlotBytes = kSB * 640;     // 16 x (128 B masks + 512 B row ids)
 
@@ -127,6 +129,7 @@ template <int PULL, int NC>
 __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
     constexpr int THREADS = 32 * (NC + 1);
     __shared__ Smem<THREADS, 1> sm;
+    constexpr int kNS = NC;
     __shared__ __align__(8) uint64_t full[kNS], empty[kNS];
     __shared__ SlotHdr hdr[kNS];
     extern __shared__ __align__(128) uint8_t ring[];  // kNS slots of kSlotBytes
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
 
 }  // namespace
 
-size_t lazy_tma_smem() { return (size_t)kNS * kSlotBytes; }
+size_t lazy_tma_smem(int consumers) { return (size_t)consumers * kSlotBytes; }
 
 void* lazy_tma_kernel(int pull, int consumers) {
     if (consumers == 8) return pull == 1 ? (void*)k_bfs_lazy_tma<1, 8> : (void*)k_bfs_lazy_tma<0, 8>;
