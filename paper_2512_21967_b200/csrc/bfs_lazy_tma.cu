@@ -62,13 +62,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_addr(bar);
     uint32_t done = 0;
-    do {
+    uint64_t t0 = 0;
+    for (uint32_t spins = 0;; ++spins) {
         asm volatile(
             "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
             : "=r"(done)
             : "r"(a), "r"(parity)
             : "memory");
-    } while (!done);
+        if (done) break;
+        if ((spins & 1023) == 0) {  // watchdog: abort the launch instead of hanging the GPU
+            uint64_t t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            if (!t0) t0 = t;
+            else if (t - t0 > 4000000000ull) __trap();
+        }
+    }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(

@@ -139,7 +139,16 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
         } else {
             // relaxed spin (an acquire load per iteration would invalidate the SM's L1
             // under the CTAs still working); one acquire fence after the exit
-            while (ld_relaxed_gpu(&bar[1]) == g) __nanosleep(32);
+            uint64_t t0 = 0;
+            for (uint32_t spins = 0; ld_relaxed_gpu(&bar[1]) == g; ++spins) {
+                __nanosleep(32);
+                if ((spins & 1023) == 0) {  // watchdog: abort instead of hanging the GPU
+                    uint64_t t;
+                    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                    if (!t0) t0 = t;
+                    else if (t - t0 > 8000000000ull) __trap();
+                }
+            }
         }
         __threadfence();
     }
