@@ -389,6 +389,10 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     }
     int per_sm = 0;
+    if (!lazy_tma) {  // small shared footprint: give the rest of the SM's 256 KB to L1
+        const char* co = getenv("BLEST_CARVEOUT");
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, co ? atoi(co) : 0));
+    }
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dyn));
     if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
     // Lazy: give each co-resident CTA an equal share of the SM's shared memory for the

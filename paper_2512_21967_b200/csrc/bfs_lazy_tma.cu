@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
                     }
                     const uint32_t myv = __shfl_sync(0xffffffffu, win.b, l) +
                                          (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
-                    const uint32_t mya = (lane < cnt) ? __shfl_sync(0xffffffffu, win.alpha, l) : 0u;
+                    const uint32_t la = __shfl_sync(0xffffffffu, win.alpha, l);  // all lanes shuffle
+                    const uint32_t mya = (lane < cnt) ? la : 0u;
                     // runs of consecutive VSS ids become one bulk copy each
                     const uint32_t prevv = __shfl_up_sync(0xffffffffu, myv, 1);
                     const bool start = lane < cnt && (lane == 0 || prevv + 1 != myv);
