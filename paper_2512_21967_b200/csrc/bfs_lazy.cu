@@ -127,37 +127,28 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
                         rw[j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
                     }
                 }
-                // Three phases over the whole batch so every dependent load of the batch
-                // is in flight at once: (1) AND with α and issue all V_curr loads,
-                // (2) V_next loads for the not-yet-visited, (3) REDs.
-                uint32_t vw[kBatch][4];
 #pragma unroll
                 for (int j = 0; j < kBatch; ++j) {
+                    if (ej[j] == kNoEntry) continue;  // warp-uniform
                     uint32_t cnt[4];
                     column_counts<PULL>(mk[j], (uint32_t)((ej[j] >> 32) & 0xFFu), cnt);
-                    const uint32_t u4[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                    // visited before this level? (V_curr, frozen; hub prefix from smem)
+                    uint32_t vw[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        bool need = cnt[c] != 0 && ej[j] != kNoEntry;
-                        if (need && u4[c] < hub_n) need = !((hub[u4[c] >> 5] >> (u4[c] & 31)) & 1u);
-                        vw[j][c] = (need && !(p.xflags & 1)) ? Vc[u4[c] >> 5] : (need ? 0u : ~0u);
+                        bool need = cnt[c] != 0;
+                        if (need && u[c] < hub_n) need = !((hub[u[c] >> 5] >> (u[c] & 31)) & 1u);
+                        vw[c] = (need && !(p.xflags & 1)) ? Vc[u[c] >> 5] : (need ? 0u : ~0u);
                     }
-                }
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    const uint32_t u4[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                    // not yet: already marked this level by anyone? (V_next at L2)
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
-                        if (!((vw[j][c] >> (u4[c] & 31)) & 1u) && !(p.xflags & 2))
-                            vw[j][c] = ld_l2_u32(Vn + (u4[c] >> 5));
-                }
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    const uint32_t u4[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+                        if (!((vw[c] >> (u[c] & 31)) & 1u) && !(p.xflags & 2)) vw[c] = ld_l2_u32(Vn + (u[c] >> 5));
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        if (!((vw[j][c] >> (u4[c] & 31)) & 1u)) {
-                            red_or(Vn + (u4[c] >> 5), 1u << (u4[c] & 31));
+                        if (!((vw[c] >> (u[c] & 31)) & 1u)) {
+                            red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
                             ++ctr[2];
                         }
                     }
