@@ -373,7 +373,7 @@ BfsEngine::~BfsEngine() {
 void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (src >= b_.n) throw InvalidArgument("bfs source out of range");
     const char* var_env = getenv("BLEST_LAZY_VARIANT");
-    const bool lazy_tma = opt.mode == Mode::Lazy && !(opt.lazy_plain || (var_env && std::string(var_env) == "plain"));
+    const bool lazy_tma = opt.mode == Mode::Lazy && (opt.lazy_tma || (var_env && std::string(var_env) == "tma"));
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
     const int consumers = nc_env ? atoi(nc_env) : 8;
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);

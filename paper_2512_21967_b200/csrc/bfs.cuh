@@ -20,7 +20,7 @@ struct EngineOptions {
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
     bool hub_cache = false;   // lazy (plain variant): stage the hub prefix of V_curr in smem
-    bool lazy_plain = false;  // lazy: register-pipelined kernel instead of the TMA pipeline
+    bool lazy_tma = false;    // lazy: TMA producer/consumer pipeline (measured slower on C2)
 };
 
 // One row per level, same fields as LevelTrace (R:include/blest/bfs_engine.hpp:27-37).

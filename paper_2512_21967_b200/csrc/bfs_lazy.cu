@@ -9,15 +9,12 @@
 // (frozen during the stage, L1-cached) and, if clear, V_next at L2; only then a
 // fire-and-forget RED sets the V_next bit (legal per SURVEY §8(a) pitfall 7).
 //
-// Stage 2 (word sweep, :296-338). Each CTA owns a contiguous chunk of the ⌈n/32⌉ words.
-// Pass A: diff = V_next & ~V_curr, V_curr |= diff, diff words kept, levels written with
-// one coalesced 128 B store per changed word, and the chunk's VSS count reduced. The CTA
-// publishes its count (tagged with the level, so no reset) and sums its predecessors';
-// pass B expands its sets' VSS ranges [real_ptrs[s], real_ptrs[s+1]) at that offset,
-// each warp writing its items' ranges with all 32 lanes (a hub set with thousands of
-// VSSs costs one warp a few µs, not one thread). The next queue is in ascending
-// slice-set order (deterministic; stage 1 then streams the BVSS in address order) and
-// no contended atomic is involved.
+// Stage 2 (word sweep, :296-338) is lazy_stage2 (bfs_device.cuh): balanced, no contended
+// atomics; it emits the next queue as the ascending list SL of active slice sets (set id,
+// first queue position). The next level first expands SL into the materialised queue —
+// every warp writes an equal contiguous share of positions, resolving sets with a
+// 32-set window in its lanes — then a grid barrier, then stage 1. A hub set with
+// thousands of VSSs is thus spread over all warps instead of one.
 #include "bfs.cuh"
 #include "bfs_device.cuh"
 
@@ -26,10 +23,12 @@ namespace blestgpu {
 namespace {
 using namespace bfsdev;
 
-constexpr unsigned long long kTagMask = (1ull << 40) - 1;
 
 template <int PULL, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
+#ifndef BLEST_MINB
+#define BLEST_MINB 1
+#endif
+__global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)) k_bfs_lazy(Params p) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
     extern __shared__ uint32_t hub[];  // optional: V_curr bits of the hub prefix
@@ -57,15 +56,17 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
         const uint32_t seed = (w == src_word) ? src_bit : 0u;
         Vc[w] = seed;
         Vn[w] = seed;
+        Fd[w] = seed;  // α of the source's set for level 1
     }
-    {
-        const unsigned long long aux = (unsigned long long)(1u << (src & 7)) << 32;
-        for (uint64_t i = gtid; i < seed_e - seed_b; i += gthreads) p.Q1[i] = aux | (seed_b + i);
+    if (threadIdx.x == 0) {
+        p.agg[blockIdx.x] = 0;
+        p.aggS[blockIdx.x] = 0;
     }
-    if (threadIdx.x == 0) p.agg[blockIdx.x] = 0;
     if (gtid == 0) {
-        p.ctl[0] = seed_e - seed_b;  // queue length of the level
-        for (int i = 1; i < 8; ++i) p.ctl[i] = 0;
+        p.SL[0] = sset;                        // first position 0
+        p.ctl[0] = seed_e - seed_b;            // T: VSSs queued for the level
+        p.ctl[1] = (seed_e > seed_b) ? 1 : 0;  // S: slice sets queued
+        for (int i = 2; i < 8; ++i) p.ctl[i] = 0;
         for (int i = 0; i < 8; ++i) p.trace[i] = 0;
     }
     grid_barrier(p.bar, gen);
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
     uint32_t level = 1;
     for (;; ++level) {
         const unsigned long long len = ld_relaxed_gpu_u64(&p.ctl[0]);
+        const uint32_t S = (uint32_t)ld_relaxed_gpu_u64(&p.ctl[1]);
         if (len == 0) break;
         if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
             if (gtid == 0) p.ctl[6] = 1;
@@ -90,8 +92,35 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
             if (level < p.trace_cap)
                 for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
         }
-        const unsigned long long* Qc = (level & 1) ? p.Q1 : p.Q0;
-        unsigned long long* Qn = (level & 1) ? p.Q0 : p.Q1;
+        unsigned long long* Qc = p.Q0;
+        // ---- expand SL into the queue: equal contiguous share per warp ----
+        {
+            const uint64_t lo = (uint64_t)gw * len / all_warps, hi = (uint64_t)(gw + 1) * len / all_warps;
+            if (lo < hi) {
+                const uint8_t* Fd8 = reinterpret_cast<const uint8_t*>(Fd);
+                SetWindow win;
+                load_window(p, Fd8, find_set(p, S, lo), S, len, win);
+                for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
+                    if (c0 + 31 >= win.wend && win.wend < len) {  // slide to the set holding c0
+                        const unsigned own = __ballot_sync(0xffffffffu, win.first <= c0);
+                        const uint32_t nb = (c0 >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
+                        load_window(p, Fd8, nb, S, len, win);
+                    }
+                    const uint64_t q = c0 + lane;
+                    int l = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint64_t f = __shfl_sync(0xffffffffu, win.first, l + step);
+                        if (f <= q) l += step;
+                    }
+                    const uint32_t v = __shfl_sync(0xffffffffu, win.b, l) +
+                                       (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
+                    const uint32_t a = __shfl_sync(0xffffffffu, win.alpha, l);
+                    if (q < hi) Qc[q] = ((unsigned long long)a << 32) | v;
+                }
+            }
+        }
+        grid_barrier(p.bar, gen);
         const bool hubs = p.hub_words && len >= p.dense_min;
         const uint32_t hub_n = hubs ? 32u * p.hub_words : 0u;
         if (hubs) {
@@ -157,91 +186,7 @@ __global__ void __launch_bounds__(THREADS) k_bfs_lazy(Params p) {
         }
         level_barrier(p, sm, gen, level, ctr, 1);
 
-        // ---- stage 2: chunked word sweep ----
-        const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
-        const uint64_t w0 = (uint64_t)blockIdx.x * per;
-        const uint64_t w1 = min(w0 + per, p.words);
-        unsigned long long my_vss = 0;
-        // pass A: diff, V_curr update, levels, VSS count of the sets to enqueue
-        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-            const uint64_t w = wb + threadIdx.x;
-            uint32_t diff = 0;
-            if (w < w1) {
-                const uint32_t nx = Vn[w];
-                diff = nx & ~Vc[w];
-                Fd[w] = diff;
-                if (diff) Vc[w] = nx;
-                for (uint32_t d = diff; d;) {
-                    const int bsel = (__ffs(d) - 1) >> 3;
-                    d &= ~(0xFFu << (8 * bsel));
-                    const uint64_t ss = 4 * w + bsel;
-                    my_vss += p.rp[ss + 1] - p.rp[ss];
-                }
-            }
-            ctr[0] += __popc(diff);
-            const uint64_t wwarp = wb + 32 * warp;
-            unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
-            while (ball) {
-                const int k = __ffs(ball) - 1;
-                ball &= ball - 1;
-                const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
-                if ((dk >> lane) & 1u) p.L[32 * (wwarp + k) + lane] = level;
-            }
-        }
-        unsigned long long cta_vss = 0;
-        block_excl_scan(sm, my_vss, &cta_vss);
-        if (threadIdx.x == 0) {
-            const unsigned long long tag = ((unsigned long long)level << 40) | cta_vss;
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag) : "memory");
-        }
-        // sum the predecessors' counts with every thread (one or two rounds of loads)
-        unsigned long long before = 0;
-        for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
-            unsigned long long x;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
-            } while ((x >> 40) != level);
-            before += x & kTagMask;
-        }
-        unsigned long long running = 0;
-        block_excl_scan(sm, before, &running);
-        if (threadIdx.x == 0 && blockIdx.x == gridDim.x - 1) p.ctl[0] = running + cta_vss;  // next length
-        if (threadIdx.x == 0) ctr[3] += (uint32_t)cta_vss;
-        // pass B: expand the chunk's sets into the queue, slice-set order; warp-cooperative
-        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-            const uint64_t w = wb + threadIdx.x;
-            const uint32_t diff = (w < w1) ? Fd[w] : 0u;
-            uint32_t b[4], c4[4];
-            unsigned long long cnt = 0;
-#pragma unroll
-            for (int bsel = 0; bsel < 4; ++bsel) {
-                b[bsel] = c4[bsel] = 0;
-                if ((diff >> (8 * bsel)) & 0xFFu) {
-                    const uint64_t ss = 4 * w + bsel;
-                    b[bsel] = p.rp[ss];
-                    c4[bsel] = p.rp[ss + 1] - b[bsel];
-                    cnt += c4[bsel];
-                }
-            }
-            unsigned long long it_total = 0;
-            unsigned long long pos = running + block_excl_scan(sm, cnt, &it_total);
-            unsigned ball = __ballot_sync(0xffffffffu, cnt != 0);
-            while (ball) {
-                const int k = __ffs(ball) - 1;
-                ball &= ball - 1;
-                unsigned long long at = __shfl_sync(0xffffffffu, pos, k);
-                const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
-#pragma unroll
-                for (int bsel = 0; bsel < 4; ++bsel) {
-                    const uint32_t bb = __shfl_sync(0xffffffffu, b[bsel], k);
-                    const uint32_t cc = __shfl_sync(0xffffffffu, c4[bsel], k);
-                    const unsigned long long aux = (unsigned long long)((dk >> (8 * bsel)) & 0xFFu) << 32;
-                    for (uint32_t t = lane; t < cc; t += 32) Qn[at + t] = aux | (bb + t);
-                    at += cc;
-                }
-            }
-            running += it_total;
-        }
+        lazy_stage2<THREADS>(p, sm, level, ctr);
         level_barrier(p, sm, gen, level, ctr, 2);
     }
     if (gtid == 0) p.ctl[4] = level - 1;

@@ -33,7 +33,6 @@ namespace blestgpu {
 namespace {
 using namespace bfsdev;
 
-constexpr unsigned long long kTagMask = (1ull << 40) - 1;
 constexpr int kSB = 16;                        // VSSs per ring slot
 // Ring slots per CTA = consumer warps: stage g uses slot g % NC and consumer g % NC, so
 // every slot is only ever refilled for the warp that emptied it (a consumer can never
@@ -84,53 +83,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
-}
-
-// One warp's view of 32 consecutive SL entries.
-struct SetWindow {
-    uint32_t base;   // SL index held by lane 0
-    uint64_t first;  // lane's first queue position (UINT64_MAX past the list)
-    uint32_t b;      // lane's first VSS id (real_ptrs[s])
-    uint32_t alpha;  // lane's frontier byte
-    uint64_t wend;   // one past the last position covered by the window
-};
-
-__device__ __forceinline__ void load_window(const Params& p, const uint8_t* Fd8, uint32_t base, uint32_t S,
-                                            uint64_t T, SetWindow& w) {
-    const unsigned lane = lane_id();
-    const uint32_t k = base + lane;
-    uint64_t first = ~0ull, nxt = T;
-    uint32_t b = 0, alpha = 0;
-    if (k < S) {
-        const unsigned long long e = p.SL[k];
-        first = e >> 32;
-        const uint32_t ss = (uint32_t)e;
-        b = p.rp[ss];
-        alpha = Fd8[ss];
-        if (lane == 31 && k + 1 < S) nxt = p.SL[k + 1] >> 32;
-    }
-    w.base = base;
-    w.first = first;
-    w.b = b;
-    w.alpha = alpha;
-    w.wend = (base + 32 < S) ? __shfl_sync(0xffffffffu, nxt, 31) : T;
-}
-
-// Largest SL index k with first(k) <= pos (first(0) = 0, entries ascending).
-__device__ __forceinline__ uint32_t find_set(const Params& p, uint32_t S, uint64_t pos) {
-    const unsigned lane = lane_id();
-    uint32_t lo = 0, hi = S;
-    while (hi - lo > 32) {
-        const uint32_t step = (hi - lo + 31) / 32;
-        const uint32_t idx = lo + lane * step;
-        const bool ok = idx < hi && (p.SL[idx] >> 32) <= pos;
-        const unsigned ball = __ballot_sync(0xffffffffu, ok);
-        lo = lo + (31 - __clz(ball)) * step;
-        hi = min(hi, lo + step);
-    }
-    const uint32_t idx = lo + lane;
-    const bool ok = idx < hi && (p.SL[idx] >> 32) <= pos;
-    return lo + (31 - __clz(__ballot_sync(0xffffffffu, ok)));
 }
 
 template <int PULL, int NC>
@@ -306,96 +258,7 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
         ring_base += nst;
         level_barrier(p, sm, gen, level, ctr, 1);
 
-        // ---- stage 2: chunked word sweep ----
-        const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
-        const uint64_t w0 = (uint64_t)blockIdx.x * per;
-        const uint64_t w1 = min(w0 + per, p.words);
-        unsigned long long my_vss = 0, my_sets = 0;
-        // pass A
-        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-            const uint64_t w = wb + threadIdx.x;
-            uint32_t diff = 0;
-            if (w < w1) {
-                const uint32_t nx = Vn[w];
-                diff = nx & ~Vc[w];
-                Fd[w] = diff;
-                if (diff) Vc[w] = nx;
-                for (uint32_t d = diff; d;) {
-                    const int bsel = (__ffs(d) - 1) >> 3;
-                    d &= ~(0xFFu << (8 * bsel));
-                    const uint64_t ss = 4 * w + bsel;
-                    const uint32_t c = p.rp[ss + 1] - p.rp[ss];
-                    my_vss += c;
-                    my_sets += c != 0;  // sets without VSSs push nothing
-                }
-            }
-            ctr[0] += __popc(diff);
-            const uint64_t wwarp = wb + 32 * warp;
-            unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
-            while (ball) {
-                const int k = __ffs(ball) - 1;
-                ball &= ball - 1;
-                const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
-                if ((dk >> lane) & 1u) p.L[32 * (wwarp + k) + lane] = level;
-            }
-        }
-        unsigned long long cta_vss = 0, cta_sets = 0;
-        block_excl_scan(sm, my_vss, &cta_vss);
-        block_excl_scan(sm, my_sets, &cta_sets);
-        if (threadIdx.x == 0) {
-            const unsigned long long tag = (unsigned long long)level << 40;
-            p.aggS[blockIdx.x] = tag | cta_sets;
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag | cta_vss)
-                         : "memory");
-        }
-        unsigned long long bv = 0, bs = 0;
-        for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
-            unsigned long long x;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
-            } while ((x >> 40) != level);
-            bv += x & kTagMask;
-            bs += ld_relaxed_gpu_u64(p.aggS + c) & kTagMask;
-        }
-        unsigned long long run_vss = 0, run_sets = 0;
-        block_excl_scan(sm, bv, &run_vss);
-        block_excl_scan(sm, bs, &run_sets);
-        if (threadIdx.x == 0) {
-            ctr[3] += (uint32_t)cta_vss;
-            if (blockIdx.x == gridDim.x - 1) {  // grid totals: the next level's T, S
-                p.ctl[0] = run_vss + cta_vss;
-                p.ctl[1] = run_sets + cta_sets;
-            }
-        }
-        // pass B: SL entries of the chunk's active sets, ascending
-        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-            const uint64_t w = wb + threadIdx.x;
-            const uint32_t diff = (w < w1) ? Fd[w] : 0u;
-            unsigned long long nv = 0, ns = 0;
-            uint32_t cnts[4];
-#pragma unroll
-            for (int bsel = 0; bsel < 4; ++bsel) {
-                cnts[bsel] = 0;
-                if ((diff >> (8 * bsel)) & 0xFFu) {
-                    const uint64_t ss = 4 * w + bsel;
-                    cnts[bsel] = p.rp[ss + 1] - p.rp[ss];
-                    nv += cnts[bsel];
-                    ns += cnts[bsel] != 0;
-                }
-            }
-            unsigned long long it_v = 0, it_s = 0;
-            unsigned long long pv = run_vss + block_excl_scan(sm, nv, &it_v);
-            unsigned long long ps = run_sets + block_excl_scan(sm, ns, &it_s);
-#pragma unroll
-            for (int bsel = 0; bsel < 4; ++bsel) {
-                if (cnts[bsel]) {
-                    p.SL[ps++] = (pv << 32) | (4 * w + bsel);
-                    pv += cnts[bsel];
-                }
-            }
-            run_vss += it_v;
-            run_sets += it_s;
-        }
+        lazy_stage2<THREADS>(p, sm, level, ctr);
         level_barrier(p, sm, gen, level, ctr, 2);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
