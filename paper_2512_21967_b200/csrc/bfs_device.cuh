@@ -12,10 +12,6 @@ namespace bfsdev {
 #define BLEST_KBATCH 4
 #endif
 constexpr int kBatch = BLEST_KBATCH;  // VSSs in flight per warp
-#ifndef BLEST_PBATCH
-#define BLEST_PBATCH 2
-#endif
-constexpr int kPB = BLEST_PBATCH;  // lazy pipelined stage 1: VSSs per pipeline stage (2 stages)
 constexpr int kPushCap = 64;      // per-warp push buffer entries (eager)
 constexpr unsigned long long kNoEntry = ~0ull;
 

@@ -131,42 +131,37 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         }
 
         // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
-        // Software-pipelined: the BVSS loads of batch k+1 (and the queue entries of batch
-        // k+2) are issued before the visited checks of batch k, so the HBM stream never
-        // waits behind the L2 round trips of the checks.
         if (gw < NW) {
-            const uint64_t stride = (uint64_t)NW * kPB;
-            auto fetch_entries = [&](uint64_t base) -> unsigned long long {
-                unsigned long long e = kNoEntry;
-                if (lane < kPB) {
-                    const uint64_t pos = base + (uint64_t)lane * NW;
-                    if (pos < len) e = Qc[pos];
+            // queue entries of the next batch are fetched while this batch is processed
+            unsigned long long e_next = kNoEntry;
+            if (lane < kBatch && gw + (uint64_t)lane * NW < len) e_next = Qc[gw + (uint64_t)lane * NW];
+            for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
+                const unsigned long long e = e_next;
+                e_next = kNoEntry;
+                if (lane < kBatch) {
+                    const uint64_t pos = p0 + (uint64_t)NW * kBatch + (uint64_t)lane * NW;
+                    if (pos < len) e_next = Qc[pos];
                 }
-                return e;
-            };
-            uint32_t mk[2][kPB];
-            uint4 rw[2][kPB];
-            unsigned long long ej[2][kPB];
-            auto issue = [&](int buf, unsigned long long e) {
+                uint32_t mk[kBatch];
+                uint4 rw[kBatch];
+                unsigned long long ej[kBatch];
 #pragma unroll
-                for (int j = 0; j < kPB; ++j) {
-                    ej[buf][j] = __shfl_sync(0xffffffffu, e, j);
-                    mk[buf][j] = 0;
-                    rw[buf][j] = make_uint4(0, 0, 0, 0);
-                    if (ej[buf][j] != kNoEntry) {
-                        const uint64_t v = (uint32_t)ej[buf][j];
-                        mk[buf][j] = ld_stream_u32(p.masks + 32 * v + lane, pol);
-                        rw[buf][j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
+                for (int j = 0; j < kBatch; ++j) {
+                    ej[j] = __shfl_sync(0xffffffffu, e, j);
+                    mk[j] = 0;
+                    rw[j] = make_uint4(0, 0, 0, 0);
+                    if (ej[j] != kNoEntry) {
+                        const uint64_t v = (uint32_t)ej[j];
+                        mk[j] = ld_stream_u32(p.masks + 32 * v + lane, pol);
+                        rw[j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
                     }
                 }
-            };
-            auto process = [&](int buf) {
 #pragma unroll
-                for (int j = 0; j < kPB; ++j) {
-                    if (ej[buf][j] == kNoEntry) continue;  // warp-uniform
+                for (int j = 0; j < kBatch; ++j) {
+                    if (ej[j] == kNoEntry) continue;  // warp-uniform
                     uint32_t cnt[4];
-                    column_counts<PULL>(mk[buf][j], (uint32_t)((ej[buf][j] >> 32) & 0xFFu), cnt);
-                    const uint32_t u[4] = {rw[buf][j].x, rw[buf][j].y, rw[buf][j].z, rw[buf][j].w};
+                    column_counts<PULL>(mk[j], (uint32_t)((ej[j] >> 32) & 0xFFu), cnt);
+                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
                     // visited before this level? (V_curr, frozen; hub prefix from smem)
                     uint32_t vw[4];
 #pragma unroll
@@ -187,20 +182,6 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                         }
                     }
                 }
-            };
-            // two-stage ring with compile-time buffer indices (kept in registers)
-            unsigned long long e_next = fetch_entries(gw + stride);
-            issue(0, fetch_entries(gw));
-            for (uint64_t p0 = gw; p0 < len; p0 += 2 * stride) {
-                unsigned long long e = e_next;
-                e_next = fetch_entries(p0 + 2 * stride);
-                issue(1, e);  // batch k+1 in flight while batch k is checked
-                process(0);
-                if (p0 + stride >= len) break;
-                e = e_next;
-                e_next = fetch_entries(p0 + 3 * stride);
-                issue(0, e);
-                process(1);
             }
         }
         level_barrier(p, sm, gen, level, ctr, 1);
