@@ -39,309 +39,13 @@ namespace blestgpu {
 
 extern std::atomic<uint64_t> g_launches;
 
+void* eager_kernel(int pull, int threads);       // bfs_eager.cu
 void* lazy_kernel(int pull, int threads);        // bfs_lazy.cu (register-pipelined variant)
 void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
 size_t lazy_tma_smem(int consumers);
 
 namespace {
 using namespace bfsdev;
-
-template <int MODE, int PULL, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_bfs(Params p) {
-    constexpr int WPC = THREADS / 32;
-    __shared__ Smem<THREADS, MODE> sm;
-    extern __shared__ uint32_t hub[];  // lazy: V_curr bits of the hub prefix [0, 32*hub_words)
-    const unsigned lane = lane_id();
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
-    const uint64_t gthreads = (uint64_t)gridDim.x * THREADS;
-    const uint32_t gw = blockIdx.x * WPC + warp;
-    const uint32_t all_warps = gridDim.x * WPC;
-    const uint32_t NW = (p.num_warps && p.num_warps < all_warps) ? p.num_warps : all_warps;
-    unsigned gen = 0;
-    const uint64_t pol = evict_first_policy();
-    if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
-    uint32_t* Vc = p.B0;  // lazy V_curr: frozen during stage 1 (L1-cacheable)
-    uint32_t* Vn = p.B1;  // lazy V_next: REDs at L2, read with L1-bypassing loads
-
-    // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
-    const uint32_t src = p.src;
-    const uint32_t sset = src / kSigma;
-    const uint32_t seed_b = p.rp[sset], seed_e = p.rp[sset + 1];
-    for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
-    const uint32_t src_word = src >> 5, src_bit = 1u << (src & 31);
-    for (uint64_t w = gtid; w < p.words; w += gthreads) {
-        const uint32_t seed = (w == src_word) ? src_bit : 0u;
-        if (MODE == 0) {
-            p.B0[w] = 0;
-            p.B1[w] = seed;  // F[1] = F_curr of level 1
-            p.B2[w] = 0;
-        } else {
-            Vc[w] = seed;
-            Vn[w] = seed;
-        }
-    }
-    {
-        unsigned long long* Q1 = p.Q1;
-        const unsigned long long aux =
-            (MODE == 0) ? ((unsigned long long)sset << 32)
-                        : ((unsigned long long)(1u << (src & 7)) << 32);
-        for (uint64_t i = gtid; i < seed_e - seed_b; i += gthreads) Q1[i] = aux | (seed_b + i);
-    }
-    if (threadIdx.x == 0) p.agg[blockIdx.x] = 0;  // stage-2 tags are per run
-    if (gtid == 0) {
-        p.ctl[0] = 0;
-        p.ctl[1] = seed_e - seed_b;
-        p.ctl[2] = 0;
-        p.ctl[3] = 0;
-        p.ctl[4] = 0;
-        p.ctl[5] = 0;
-        p.ctl[6] = 0;
-        for (int i = 0; i < 8; ++i) p.trace[i] = 0;
-    }
-    grid_barrier(p.bar, gen);
-
-    unsigned long long* pbuf = sm.push[warp];
-    uint32_t pcount = 0;
-    uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
-    uint32_t level = 1;
-    for (;; ++level) {
-        const unsigned long long len = ld_relaxed_gpu_u64(&p.ctl[level & 3]);
-        if (len == 0) break;
-        if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
-            if (gtid == 0) p.ctl[6] = 1;
-            break;
-        }
-        if (gtid == 0) {
-            p.ctl[(level + 2) & 3] = 0;
-            if (level - 1 < p.trace_cap) {
-                p.trace[8ull * (level - 1) + 0] = level;
-                p.trace[8ull * (level - 1) + 1] = len;
-                p.tstamp[3ull * (level - 1)] = globaltimer();
-            } else {
-                atomicAdd(&p.trace[8ull * (p.trace_cap - 1) + 1], len);
-            }
-            if (level < p.trace_cap)
-                for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
-        }
-        unsigned long long* Qc = queue_at<MODE>(p, level);
-        unsigned long long* Qn = queue_at<MODE>(p, level + 1);
-        unsigned long long* qlen_next = &p.ctl[(level + 1) & 3];
-        const uint32_t* Fc = (MODE == 0) ? fbuf(p, level) : nullptr;
-        uint32_t* Fn = (MODE == 0) ? fbuf(p, level + 1) : nullptr;
-
-        if (MODE == 0) {
-            // Zero the frontier bytes level ℓ-1 read: they become F_next at ℓ+1.
-            uint8_t* Fz = reinterpret_cast<uint8_t*>(fbuf(p, level + 2));
-            const unsigned long long* Qz = queue_at<MODE>(p, level + 2);
-            const unsigned long long zlen = ld_relaxed_gpu_u64(&p.ctl[(level + 3) & 3]);
-            for (uint64_t i = gtid; i < zlen; i += gthreads) Fz[Qz[i] >> 32] = 0;
-        }
-
-        // ---- pull over the queue (pull_vss, R:src/bfs_engine.cpp:131-146) ----
-        // Dense lazy levels: stage the frozen V_curr bits of the hub prefix in shared memory,
-        // so the visited test of the (mostly hub-bound) hits is served on-chip.
-        const bool hubs = (MODE == 1) && p.hub_words && len >= p.dense_min;
-        const uint32_t hub_n = hubs ? 32u * p.hub_words : 0u;
-        if (hubs) {
-            const uint4* src4 = reinterpret_cast<const uint4*>(Vc);
-            uint4* dst4 = reinterpret_cast<uint4*>(hub);
-            for (uint32_t i = threadIdx.x; i < p.hub_words / 4; i += THREADS) dst4[i] = src4[i];
-            __syncthreads();
-        }
-        if (gw < NW) {
-            for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
-                unsigned long long e = kNoEntry;
-                if (lane < kBatch) {
-                    const uint64_t pos = p0 + (uint64_t)lane * NW;
-                    if (pos < len) e = Qc[pos];
-                }
-                uint32_t alpha_l = 0;
-                if (MODE == 0 && e != kNoEntry) {
-                    const uint32_t ss = (uint32_t)(e >> 32);
-                    alpha_l = reinterpret_cast<const uint8_t*>(Fc)[ss];  // frontier_byte :148-151
-                }
-                uint32_t mk[kBatch];
-                uint4 rw[kBatch];
-                unsigned long long ej[kBatch];
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    ej[j] = __shfl_sync(0xffffffffu, e, j);
-                    mk[j] = 0;
-                    rw[j] = make_uint4(0, 0, 0, 0);
-                    if (ej[j] != kNoEntry) {
-                        const uint64_t v = (uint32_t)ej[j];
-                        mk[j] = ld_stream_u32(p.masks + 32 * v + lane, pol);
-                        rw[j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    if (ej[j] == kNoEntry) continue;  // warp-uniform
-                    const uint32_t alpha = (MODE == 0) ? __shfl_sync(0xffffffffu, alpha_l, j)
-                                                       : (uint32_t)((ej[j] >> 32) & 0xFFu);
-                    uint32_t cnt[4];
-                    column_counts<PULL>(mk[j], alpha, cnt);
-                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-                    // All four dependent state loads of this VSS are issued before any of
-                    // them is consumed (4 independent L1/L2 requests in flight per lane).
-                    if (MODE == 1) {
-                        // stage-1 sink (:286-289): relaxed OR into V_next unless the vertex
-                        // was visited before this level or is already marked this level.
-                        // visited before this level? (V_curr; hub prefix from shared memory)
-                        uint32_t vw[4];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            bool need = cnt[c] != 0;
-                            if (need && u[c] < hub_n) need = !((hub[u[c] >> 5] >> (u[c] & 31)) & 1u);
-                            vw[c] = (need && !(p.xflags & 1)) ? Vc[u[c] >> 5] : (need ? 0u : ~0u);
-                        }
-                        // not yet: already marked this level by anyone? (V_next at L2)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (!((vw[c] >> (u[c] & 31)) & 1u) && !(p.xflags & 2)) vw[c] = ld_relaxed_gpu(Vn + (u[c] >> 5));
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            if (!((vw[c] >> (u[c] & 31)) & 1u)) {
-                                red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
-                                ++ctr[2];
-                            }
-                        }
-                    } else {
-                        // eager sink (:198-211)
-                        uint32_t lv[4];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) lv[c] = cnt[c] ? p.L[u[c]] : 0u;
-                        uint32_t old[4];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            old[c] = (lv[c] == kInf) ? atomicOr(Fn + (u[c] >> 5), 1u << (u[c] & 31))
-                                                     : 0xFFFFFFFFu;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            bool push = false;
-                            if (lv[c] == kInf) {
-                                ++ctr[1];
-                                if (!((old[c] >> (u[c] & 31)) & 1u)) {
-                                    p.L[u[c]] = level;
-                                    ++ctr[0];
-                                    push = ((old[c] >> (8 * ((u[c] >> 3) & 3))) & 0xFFu) == 0;
-                                }
-                            }
-                            push_column(p, push, (unsigned long long)(u[c] >> 3) << 32 | (u[c] >> 3), pbuf,
-                                        pcount, Qn, qlen_next, ctr[3], ctr[1]);
-                        }
-                    }
-                }
-            }
-        }
-
-        if (MODE == 1) {
-            level_barrier(p, sm, gen, level, ctr, 1);
-            // ---- stage 2 (R:src/bfs_engine.cpp:296-338): chunked word sweep ----
-            uint32_t* Fd = p.B2;  // this level's diff words (the reference's F_curr, :310-311)
-            const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
-            const uint64_t w0 = (uint64_t)blockIdx.x * per;
-            const uint64_t w1 = min(w0 + per, p.words);
-            unsigned long long mine = 0;
-            // pass A: diff, V_curr update, levels, VSS count of the sets to enqueue
-            for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-                const uint64_t w = wb + threadIdx.x;
-                uint32_t diff = 0;
-                if (w < w1) {
-                    const uint32_t nx = Vn[w];
-                    diff = nx & ~Vc[w];
-                    Fd[w] = diff;
-                    if (diff) Vc[w] = nx;
-                    for (uint32_t d = diff; d; ) {
-                        const int bsel = (__ffs(d) - 1) >> 3;
-                        d &= ~(0xFFu << (8 * bsel));
-                        const uint64_t ss = 4 * w + bsel;
-                        mine += p.rp[ss + 1] - p.rp[ss];
-                    }
-                }
-                ctr[0] += __popc(diff);
-                const uint64_t wwarp = wb + 32 * warp;  // this warp's 32 words
-                unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
-                while (ball) {
-                    const int k = __ffs(ball) - 1;
-                    ball &= ball - 1;
-                    const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
-                    if ((dk >> lane) & 1u) p.L[32 * (wwarp + k) + lane] = level;
-                }
-            }
-            unsigned long long cta_total = 0;
-            block_excl_scan(sm, mine, &cta_total);
-            // publish this CTA's count, then sum the predecessors' (level-tagged)
-            if (threadIdx.x == 0) {
-                const unsigned long long tag = ((unsigned long long)level << 40) | cta_total;
-                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag) : "memory");
-            }
-            if (warp == 0) {
-                unsigned long long before = 0;
-                for (uint32_t c = lane; c < blockIdx.x; c += 32) {
-                    unsigned long long x;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
-                    } while ((x >> 40) != level);
-                    before += x & ((1ull << 40) - 1);
-                }
-                before = warp_sum(before);
-                if (lane == 0) {
-                    sm.base = before;
-                    if (blockIdx.x == gridDim.x - 1) *qlen_next = before + cta_total;
-                }
-            }
-            __syncthreads();
-            // pass B: expand the chunk's slice sets into the queue, in slice-set order
-            unsigned long long running = sm.base;
-            for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-                const uint64_t w = wb + threadIdx.x;
-                const uint32_t diff = (w < w1) ? Fd[w] : 0u;
-                uint32_t b[4], e[4];
-                unsigned long long cnt = 0;
-#pragma unroll
-                for (int bsel = 0; bsel < 4; ++bsel) {
-                    b[bsel] = e[bsel] = 0;
-                    if ((diff >> (8 * bsel)) & 0xFFu) {
-                        const uint64_t ss = 4 * w + bsel;
-                        b[bsel] = p.rp[ss];
-                        e[bsel] = p.rp[ss + 1];
-                        cnt += e[bsel] - b[bsel];
-                    }
-                }
-                unsigned long long it_total = 0;
-                unsigned long long pos = running + block_excl_scan(sm, cnt, &it_total);
-#pragma unroll
-                for (int bsel = 0; bsel < 4; ++bsel) {
-                    const unsigned long long aux = (unsigned long long)((diff >> (8 * bsel)) & 0xFFu) << 32;
-                    for (uint32_t v = b[bsel]; v < e[bsel]; ++v) Qn[pos++] = aux | v;
-                }
-                running += it_total;
-            }
-            if (threadIdx.x == 0) ctr[3] += (uint32_t)cta_total;
-        }
-        if (MODE == 0 && pcount) {
-            const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next);
-            if (lane == 0) {
-                ctr[3] += t;
-                ctr[1] += 1;
-            }
-        }
-        level_barrier(p, sm, gen, level, ctr, 2);
-    }
-    if (gtid == 0) p.ctl[4] = level - 1;
-}
-
-template <int MODE, int PULL>
-void* pick_kernel(int threads) {
-    switch (threads) {
-        case 256: return (void*)k_bfs<MODE, PULL, 256>;
-        case 512: return (void*)k_bfs<MODE, PULL, 512>;
-        case 1024: return (void*)k_bfs<MODE, PULL, 1024>;
-    }
-    throw InvalidArgument("threads per CTA must be 256, 512 or 1024");
-}
 
 }  // namespace
 
@@ -350,14 +54,14 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     const uint64_t levels_bound = (uint64_t)b.n + 2;
     trace_cap_ = (uint32_t)std::min<uint64_t>(levels_bound, 1u << 20);
     levels_.alloc(b.n ? b.n : 1);
-    bits_.alloc(3 * (words_ ? words_ : 1));
+    bits_.alloc(4 * (words_ ? words_ : 1));
     q_.alloc(3 * (uint64_t)(b.num_vss ? b.num_vss : 1));
     ctl_.alloc(8);
     agg_.alloc(4096);
     aggS_.alloc(4096);
     sl_.alloc((uint64_t)b.num_sets + 1);
     CK(cudaMemset(agg_.p, 0, 4096 * 8));
-    bar_.alloc(2);
+    bar_.alloc(4);  // count, pad, {payload | generation}
     trace_.alloc(8ull * trace_cap_);
     tstamp_.alloc(3ull * trace_cap_);
     // hub prefix staged in shared memory on dense lazy levels (opt-in): at most what one
@@ -379,7 +83,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
-        kern = opt.pull == Pull::Mma ? pick_kernel<0, 1>(threads) : pick_kernel<0, 0>(threads);
+        kern = eager_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
     else
         kern = lazy_tma ? lazy_tma_kernel(opt.pull == Pull::Mma ? 1 : 0, consumers)
                         : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
@@ -434,6 +138,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.B0 = bits_.p;
     p.B1 = bits_.p + words_;
     p.B2 = bits_.p + 2 * words_;
+    p.B3 = bits_.p + 3 * words_;
     const uint64_t qcap = b_.num_vss ? b_.num_vss : 1;
     p.Q0 = q_.p;
     p.Q1 = q_.p + qcap;
@@ -453,7 +158,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);
     cudaStream_t st = stream();
-    CK(cudaMemsetAsync(bar_.p, 0, 2 * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
     void* args[] = {&p};
     CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, dyn, st));
     last_hub_words_ = hub_words;

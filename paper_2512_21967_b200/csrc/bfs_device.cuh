@@ -25,6 +25,7 @@ struct Params {
     uint32_t* B0;  // eager F0 | lazy V_curr
     uint32_t* B1;  // eager F1 | lazy V_next
     uint32_t* B2;  // eager F2 | lazy per-level diff
+    uint32_t* B3;  // eager visited bitmap VIS
     unsigned long long* Q0;
     unsigned long long* Q1;
     unsigned long long* Q2;
@@ -204,8 +205,9 @@ __device__ __forceinline__ void column_counts(uint32_t m, uint32_t alpha, uint32
 // Flush per-thread counters into the CTA's shared counters, then (thread 0) into the
 // level's trace row; then the grid barrier; block 0 stamps the time.
 template <int THREADS, int MODE>
-__device__ __forceinline__ void level_barrier(const Params& p, Smem<THREADS, MODE>& sm, unsigned& gen,
-                                              uint32_t level, uint32_t (&c)[4], int stamp_slot) {
+__device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS, MODE>& sm, unsigned& gen,
+                                                  uint32_t level, uint32_t (&c)[4], int stamp_slot,
+                                                  const unsigned long long* payload = nullptr) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t s = warp_sum(c[i]);
@@ -226,9 +228,10 @@ __device__ __forceinline__ void level_barrier(const Params& p, Smem<THREADS, MOD
 #pragma unroll
         for (int i = 0; i < 4; ++i) sm.ctr[i] = 0;
     }
-    grid_barrier(p.bar, gen);
+    const uint32_t pay = grid_barrier_pay(p.bar, gen, payload);
     if (blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
         p.tstamp[3ull * (level - 1) + stamp_slot] = globaltimer();
+    return pay;
 }
 
 

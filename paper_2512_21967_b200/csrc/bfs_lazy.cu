@@ -69,12 +69,12 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         for (int i = 2; i < 8; ++i) p.ctl[i] = 0;
         for (int i = 0; i < 8; ++i) p.trace[i] = 0;
     }
-    grid_barrier(p.bar, gen);
+    uint32_t next_T = grid_barrier_pay(p.bar, gen, &p.ctl[0]);
 
     uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
     uint32_t level = 1;
     for (;; ++level) {
-        const unsigned long long len = ld_relaxed_gpu_u64(&p.ctl[0]);
+        const unsigned long long len = next_T;  // broadcast by the barrier
         const uint32_t S = (uint32_t)ld_relaxed_gpu_u64(&p.ctl[1]);
         if (len == 0) break;
         if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         level_barrier(p, sm, gen, level, ctr, 1);
 
         lazy_stage2<THREADS>(p, sm, level, ctr);
-        level_barrier(p, sm, gen, level, ctr, 2);
+        next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
 }

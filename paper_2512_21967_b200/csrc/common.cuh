@@ -122,39 +122,54 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
     return v;
 }
 
-// Sense-free generation barrier across the co-resident (cooperatively launched) grid.
-// bar[0] = arrival count, bar[1] = generation. Thread 0 of each CTA arrives; the last
-// arrival resets the count and bumps the generation (release); the rest spin with
-// acquire loads. __syncthreads on both sides orders the CTA's other threads.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+// Generation barrier across the co-resident (cooperatively launched) grid.
+// bar[0] = arrival count (u32); bar[2..3] = one 64-bit word {payload:32 | generation:32}.
+// Thread 0 of each CTA arrives with a release atomic; the last arrival resets the count,
+// reads the 32-bit payload (a value every CTA needs right after the barrier, e.g. the next
+// queue length — final once everyone has arrived) and publishes {payload, gen+1} with a
+// release store; the others spin on relaxed loads (tight first, then backing off) and
+// finish with an acquire fence. __syncthreads on both sides orders the CTA's threads.
+// Returns the payload to every thread.
+__device__ __forceinline__ uint32_t grid_barrier_pay(unsigned* bar, unsigned& gen, const unsigned long long* payload) {
+    __shared__ uint32_t s_pay;
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned g = gen;
-        __threadfence();
-        const unsigned arrived = atomicAdd(&bar[0], 1u);
+        unsigned long long* word = reinterpret_cast<unsigned long long*>(bar + 2);
+        unsigned arrived;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+        uint32_t pay = 0;
         if (arrived == gridDim.x - 1) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             bar[0] = 0;
-            __threadfence();
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar[1]), "r"(g + 1) : "memory");
+            if (payload) pay = (uint32_t)ld_relaxed_gpu_u64(payload);
+            const unsigned long long v = ((unsigned long long)pay << 32) | (g + 1);
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(word), "l"(v) : "memory");
         } else {
-            // relaxed spin (an acquire load per iteration would invalidate the SM's L1
-            // under the CTAs still working); one acquire fence after the exit
             uint64_t t0 = 0;
-            for (uint32_t spins = 0; ld_relaxed_gpu(&bar[1]) == g; ++spins) {
-                __nanosleep(32);
-                if ((spins & 1023) == 0) {  // watchdog: abort instead of hanging the GPU
+            unsigned long long v;
+            for (uint32_t spins = 0;; ++spins) {
+                v = ld_relaxed_gpu_u64(word);
+                if ((uint32_t)v != g) break;
+                if (spins > 64) __nanosleep(64);
+                if ((spins & 1023) == 1023) {  // watchdog: abort instead of hanging the GPU
                     uint64_t t;
                     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                     if (!t0) t0 = t;
                     else if (t - t0 > 8000000000ull) __trap();
                 }
             }
+            pay = (uint32_t)(v >> 32);
         }
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        s_pay = pay;
     }
     gen += 1;
     __syncthreads();
+    return s_pay;
 }
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) { grid_barrier_pay(bar, gen, nullptr); }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
     const unsigned lane = threadIdx.x & 31;
