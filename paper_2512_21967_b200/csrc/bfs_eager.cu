@@ -8,11 +8,13 @@
 // Queue entries are 64-bit: low = VSS id, high = slice set (saves virtual_to_real, :192);
 // α is the set's byte of F_curr (frontier_byte :148-151), loaded beside the mask/row loads.
 //
-// Sink (:198-211): a visited bitmap VIS (n bits) replaces the reference's levels[u] test —
-// one plain, L1-cacheable 4-byte load per nonzero column (stale reads are conservative);
-// if clear, atomicOr(VIS) elects the single discoverer, which stores levels[u] = ℓ and
-// atomicOrs u's bit into F_next; the first bit of a slice set in F_next this level (old
-// byte zero, :204-205) pushes the set's VSS range. Pushes gather in a per-warp shared
+// Sink (:198-211): the reference's levels[u] test becomes "VIS | F_curr" — two plain
+// 4-byte bitmap loads (2 × n/8 bytes, L1/L2-resident, unlike the 4n-byte level array):
+// VIS holds every discovery up to level ℓ-2 (level ℓ-1's discoveries are F_curr, frozen;
+// they are ORed into VIS after this level's pull — adding bits that F_curr already has,
+// so concurrent readers' union never changes). A clear test elects the discoverer with
+// one atomicOr into F_next (old bit clear), which stores levels[u] = ℓ; the first bit of
+// a slice set in F_next this level (old byte zero, :204-205) pushes the set's VSS range. Pushes gather in a per-warp shared
 // buffer; a flush reserves queue space with ONE atomicAdd per buffer (warp-aggregated
 // reservation) and expands [real_ptrs[s], real_ptrs[s+1]).
 //
@@ -30,7 +32,10 @@ namespace {
 using namespace bfsdev;
 
 template <int PULL, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_eager(Params p) {
+#ifndef BLEST_EAGER_MINB
+#define BLEST_EAGER_MINB 1
+#endif
+__global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params p) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 0> sm;
     const unsigned lane = lane_id();
@@ -56,7 +61,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_eager(Params p)
         p.B0[w] = 0;
         p.B1[w] = seed;  // F[1] = F_curr of level 1
         p.B2[w] = 0;
-        VIS[w] = seed;
+        VIS[w] = 0;  // the source is in F_curr of level 1
     }
     {
         const unsigned long long aux = (unsigned long long)sset << 32;
@@ -138,11 +143,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_eager(Params p)
                     const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
                     uint32_t vw[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) vw[c] = cnt[c] ? VIS[u[c] >> 5] : ~0u;
+                    for (int c = 0; c < 4; ++c)
+                        vw[c] = cnt[c] ? (VIS[u[c] >> 5] | reinterpret_cast<const uint32_t*>(Fc8)[u[c] >> 5]) : ~0u;
                     uint32_t old[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
-                        old[c] = ((vw[c] >> (u[c] & 31)) & 1u) ? ~0u : atomicOr(VIS + (u[c] >> 5), 1u << (u[c] & 31));
+                        old[c] = ((vw[c] >> (u[c] & 31)) & 1u) ? ~0u : atomicOr(Fn + (u[c] >> 5), 1u << (u[c] & 31));
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         bool push = false;
@@ -151,9 +157,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_eager(Params p)
                             if (!((old[c] >> (u[c] & 31)) & 1u)) {  // this lane discovered u
                                 p.L[u[c]] = level;
                                 ++ctr[0];
-                                const uint32_t of = atomicOr(Fn + (u[c] >> 5), 1u << (u[c] & 31));
-                                ++ctr[1];
-                                push = ((of >> (8 * ((u[c] >> 3) & 3))) & 0xFFu) == 0;
+                                push = ((old[c] >> (8 * ((u[c] >> 3) & 3))) & 0xFFu) == 0;
                             }
                         }
                         push_column(p, push, (unsigned long long)(u[c] >> 3) << 32 | (u[c] >> 3), pbuf, pcount,
@@ -170,6 +174,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_eager(Params p)
             }
         }
         {
+            // Merge level ℓ-1's discoveries (F_curr bytes of this queue's sets) into VIS.
+            uint8_t* VIS8 = reinterpret_cast<uint8_t*>(VIS);
+            for (uint64_t i = gtid; i < len; i += gthreads) {
+                const uint32_t ss = (uint32_t)(Qc[i] >> 32);
+                VIS8[ss] |= Fc8[ss];
+            }
             // Zero the frontier bytes level ℓ-1 read: they become F_next at ℓ+1.
             uint8_t* Fz = reinterpret_cast<uint8_t*>(fsel(k2));
             const unsigned long long* Qz = qsel(k2);
