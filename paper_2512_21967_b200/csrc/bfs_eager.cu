@@ -11,16 +11,17 @@
 // Sink (:198-211): the reference's levels[u] test becomes "VIS | F_curr" — two plain
 // 4-byte bitmap loads (2 × n/8 bytes, L1/L2-resident, unlike the 4n-byte level array):
 // VIS holds every discovery up to level ℓ-2 (level ℓ-1's discoveries are F_curr, frozen;
-// they are ORed into VIS after this level's pull — adding bits that F_curr already has,
-// so concurrent readers' union never changes). A clear test elects the discoverer with
+// they are ORed into VIS during this level's pull with a RED per dequeued VSS — adding
+// bits that F_curr already has, so concurrent readers' union never changes). A clear test elects the discoverer with
 // one atomicOr into F_next (old bit clear), which stores levels[u] = ℓ; the first bit of
 // a slice set in F_next this level (old byte zero, :204-205) pushes the set's VSS range. Pushes gather in a per-warp shared
 // buffer; a flush reserves queue space with ONE atomicAdd per buffer (warp-aggregated
 // reservation) and expands [real_ptrs[s], real_ptrs[s+1]).
 //
-// Frontier bitmaps are triple-buffered: level ℓ reads F[ℓ%3], ORs into F[(ℓ+1)%3], and —
-// after its pull — zeroes the bytes of F[(ℓ+2)%3] that level ℓ-1 read (found from queue
-// ℓ-1), so no Θ(n) clear is ever needed (the reference clears every word, :227-228).
+// Frontier bitmaps are triple-buffered: level ℓ reads F[ℓ%3], ORs into F[(ℓ+1)%3], and
+// zeroes the bytes of F[(ℓ+2)%3] that level ℓ-1 read (set ids fetched from queue ℓ-1 at
+// the level's start, stores issued after the pull), so no Θ(n) clear is ever needed
+// (the reference clears every word, :227-228) and nothing sits on the level's critical path.
 #include <atomic>
 
 #include "bfs.cuh"
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
     unsigned long long* pbuf = sm.push[warp];
     uint32_t pcount = 0;
     uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
+    unsigned long long prev_len = 0;  // length of queue ℓ-1 (its sets' F bytes get zeroed)
     uint32_t level = 1;
     for (;; ++level) {
         const unsigned long long len = next_len;
@@ -107,6 +109,11 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
         const uint8_t* Fc8 = reinterpret_cast<const uint8_t*>(fsel(k0));
         uint32_t* Fn = fsel(k1);
         unsigned long long* qlen_next = &p.ctl[(level + 1) & 3];
+        // Frontier bytes level ℓ-1 read (sets of queue ℓ-1) become F_next at ℓ+1: fetch this
+        // thread's set id now, store the zero after the pull (latency hidden by the pull).
+        uint8_t* Fz = reinterpret_cast<uint8_t*>(fsel(k2));
+        const unsigned long long* Qz = qsel(k2);
+        const uint32_t zss = (gtid < prev_len) ? (uint32_t)(Qz[gtid] >> 32) : 0xFFFFFFFFu;
 
         // ---- pull over the queue (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
@@ -120,6 +127,10 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                     if (pos < len) e_next = Qc[pos];
                 }
                 const uint32_t alpha_l = (e != kNoEntry) ? Fc8[e >> 32] : 0u;  // frontier_byte
+                if (e != kNoEntry) {  // fold level ℓ-1's discoveries of this set into VIS
+                    const uint32_t ss = (uint32_t)(e >> 32);
+                    red_or(VIS + (ss >> 2), alpha_l << (8 * (ss & 3)));
+                }
                 uint32_t mk[kBatch];
                 uint4 rw[kBatch];
                 unsigned long long ej[kBatch];
@@ -173,19 +184,9 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                 ctr[1] += 1;
             }
         }
-        {
-            // Merge level ℓ-1's discoveries (F_curr bytes of this queue's sets) into VIS.
-            uint8_t* VIS8 = reinterpret_cast<uint8_t*>(VIS);
-            for (uint64_t i = gtid; i < len; i += gthreads) {
-                const uint32_t ss = (uint32_t)(Qc[i] >> 32);
-                VIS8[ss] |= Fc8[ss];
-            }
-            // Zero the frontier bytes level ℓ-1 read: they become F_next at ℓ+1.
-            uint8_t* Fz = reinterpret_cast<uint8_t*>(fsel(k2));
-            const unsigned long long* Qz = qsel(k2);
-            const unsigned long long zlen = ld_relaxed_gpu_u64(&p.ctl[(level + 3) & 3]);
-            for (uint64_t i = gtid; i < zlen; i += gthreads) Fz[Qz[i] >> 32] = 0;
-        }
+        if (zss != 0xFFFFFFFFu) Fz[zss] = 0;
+        for (uint64_t i = gtid + gthreads; i < prev_len; i += gthreads) Fz[Qz[i] >> 32] = 0;
+        prev_len = len;
         next_len = level_barrier(p, sm, gen, level, ctr, 2, qlen_next);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
