@@ -10,5 +10,5 @@ OUT=gpurun_out
 mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_${CFG}.csv \
     python bench.py --config $CFG --mode $MODE --steps 8 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/launches_${CFG}.log 2>&1 || true
-ncu --set full --clock-control none --import-source on -k regex:k_bfs -s 12 -c 1 -o $OUT/full_${CFG} \
+ncu --set full --clock-control none --import-source on -k regex:k_bfs -s 3 -c 1 -o $OUT/full_${CFG} \
     python bench.py --config $CFG --mode $MODE --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/full_${CFG}.log 2>&1 || true
