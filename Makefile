@@ -28,4 +28,10 @@ oracle:
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean cpptest
+
+cpptest: tests/cpp/facade_test
+
+tests/cpp/facade_test: tests/cpp/facade_test.cpp include/blest_b200.hpp include/blest_b200.h $(LIB)
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ tests/cpp/facade_test.cpp -Lpaper_2512_21967_b200 -lblest_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../paper_2512_21967_b200'
