@@ -183,6 +183,25 @@ int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
 /* Launch geometry of the last run (CTAs, threads per CTA). */
 int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads);
 
+/* ---- row-partitioned multi-GPU mode (no reference counterpart) ---------- */
+/* BVSS of A[rows [row_lo, row_hi), all columns] (row_lo 32-aligned, row_hi 32-aligned or n):
+ * every column slice set keeps its VSS range, row ids stay global. One rank = one range. */
+int blest_bvss_build_rows(blest_graph g, uint32_t row_lo, uint32_t row_hi, blest_bvss* out);
+/* Owned rows and owned frontier words [word_lo, word_hi). */
+int blest_part_range(blest_bvss b, uint32_t* row_lo, uint32_t* row_hi, uint64_t* word_lo, uint64_t* word_hi);
+/* init_state for this rank (R:src/bfs_engine.cpp:30-49 restricted to owned rows). */
+int blest_part_begin(blest_bvss b, uint32_t src, uint64_t* queue_len);
+/* Stage 1 of one level over the local queue (lazy pull, R:src/bfs_engine.cpp:273-292). */
+int blest_part_pull(blest_bvss b);
+/* Stage 2 over the owned words (R:src/bfs_engine.cpp:296-338): levels written, the owned
+ * diff words stored to diff_out (device, word_hi-word_lo words) for the all-gather. */
+int blest_part_sweep(blest_bvss b, uint32_t level, uint32_t* diff_out, uint64_t* discovered);
+/* After the all-gather: queue this rank's VSSs of every active set of the full diff
+ * (device, ceil(n/32) words); total_discovered = set bits over all ranks (0 = done). */
+int blest_part_enqueue(blest_bvss b, const uint32_t* full_diff, uint64_t* queue_len, uint64_t* total_discovered);
+/* Levels of the owned rows (host, row_hi-row_lo entries). */
+int blest_part_levels(blest_bvss b, uint32_t* levels_out);
+
 #ifdef __cplusplus
 }
 #endif

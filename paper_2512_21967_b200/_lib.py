@@ -117,6 +117,13 @@ SIGNATURES = {
     "blest_bfs_levels_device": (i32, [vp, P(vp)]),
     "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),
+    "blest_bvss_build_rows": (i32, [vp, u32, u32, P(vp)]),
+    "blest_part_range": (i32, [vp, P(u32), P(u32), P(u64), P(u64)]),
+    "blest_part_begin": (i32, [vp, u32, P(u64)]),
+    "blest_part_pull": (i32, [vp]),
+    "blest_part_sweep": (i32, [vp, u32, vp, P(u64)]),
+    "blest_part_enqueue": (i32, [vp, vp, P(u64), P(u64)]),
+    "blest_part_levels": (i32, [vp, vp]),
 }
 
 _lib = None

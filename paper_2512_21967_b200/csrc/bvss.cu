@@ -13,18 +13,27 @@ namespace blestgpu {
 
 namespace {
 
+// Arcs whose target row lies outside [row_lo, row_hi) get the drop key (all ones, sorts
+// last); `kept` counts the arcs inside (the structure's m).
 __global__ void k_slice_pairs(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tgt,
-                              uint32_t n, uint64_t* __restrict__ keys, uint8_t* __restrict__ bits) {
+                              uint32_t n, uint32_t row_lo, uint32_t row_hi, uint64_t* __restrict__ keys,
+                              uint8_t* __restrict__ bits, unsigned long long* __restrict__ kept) {
     const uint32_t lane = threadIdx.x & 31;
+    unsigned long long mine = 0;
     for (uint64_t u = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; u < n;
          u += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         const uint64_t hi = (u >> 3) << 32;
         const uint8_t bit = (uint8_t)(1u << (u & 7));
         for (uint64_t i = off[u] + lane; i < off[u + 1]; i += 32) {
-            keys[i] = hi | tgt[i];
-            bits[i] = bit;
+            const uint32_t v = tgt[i];
+            const bool in = v >= row_lo && v < row_hi;
+            keys[i] = in ? (hi | v) : ~0ull;
+            bits[i] = in ? bit : (uint8_t)0;
+            mine += in;
         }
     }
+    mine = warp_sum(mine);
+    if (lane == 0 && mine) atomicAdd(kept, mine);
 }
 
 struct OrOp {
@@ -101,11 +110,16 @@ int bits_of(uint64_t x) {
 
 }  // namespace
 
-DeviceBvss bvss_build(const DeviceGraph& g) {
+DeviceBvss bvss_build(const DeviceGraph& g, uint32_t row_lo, uint32_t row_hi) {
     cudaStream_t st = stream();
+    if (row_hi > g.n) row_hi = g.n;
+    if (row_lo > row_hi) row_lo = row_hi;
+    const bool all_rows = row_lo == 0 && row_hi == g.n;
     DeviceBvss b;
     b.n = g.n;
     b.m = g.m;
+    b.row_lo = row_lo;
+    b.row_hi = row_hi;
     b.num_sets = (uint32_t)(((uint64_t)g.n + kSigma - 1) / kSigma);
     b.real_ptrs.alloc((size_t)b.num_sets + 1);
     CK(cudaMemsetAsync(b.real_ptrs.p, 0, ((size_t)b.num_sets + 1) * 4, st));
@@ -117,9 +131,18 @@ DeviceBvss bvss_build(const DeviceGraph& g) {
     // 1. (set, row) keys with the column bit, one per arc.
     DevBuf<uint64_t> keys(m);
     DevBuf<uint8_t> bits(m);
-    k_slice_pairs<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.off.p, g.tgt.p, g.n, keys.p, bits.p);
+    DevBuf<unsigned long long> kept(1);
+    CK(cudaMemsetAsync(kept.p, 0, 8, st));
+    k_slice_pairs<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.off.p, g.tgt.p, g.n, row_lo, row_hi, keys.p,
+                                                                    bits.p, kept.p);
     CK(cudaGetLastError());
-    radix_pairs(keys, bits, m, 32 + bits_of(b.num_sets));
+    radix_pairs(keys, bits, m, all_rows ? 32 + bits_of(b.num_sets) : 64);
+    if (!all_rows) {
+        unsigned long long hk = 0;
+        CK(cudaMemcpyAsync(&hk, kept.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        b.m = hk;
+    }
     // 2. OR-reduce by key -> unpadded slices, sorted by (set, row) (R:src/bvss.cpp:75-88).
     DevBuf<uint64_t> skeys(m);
     DevBuf<uint8_t> smask(m);
@@ -135,6 +158,11 @@ DeviceBvss bvss_build(const DeviceGraph& g) {
     unsigned long long ns = 0;
     CK(cudaMemcpyAsync(&ns, nsl.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (!all_rows && ns) {  // the drop keys reduce to one trailing all-ones slice
+        uint64_t last = 0;
+        CK(cudaMemcpy(&last, skeys.p + ns - 1, 8, cudaMemcpyDeviceToHost));
+        if (last == ~0ull) --ns;
+    }
     keys.release();
     bits.release();
     b.num_unpadded = ns;

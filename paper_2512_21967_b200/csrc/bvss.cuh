@@ -20,14 +20,17 @@ struct DeviceBvss {
     uint32_t num_sets = 0;
     uint32_t num_vss = 0;
     uint64_t num_unpadded = 0;
+    uint32_t row_lo = 0, row_hi = 0xFFFFFFFFu;  // rows packed (multi-GPU partition), else all
     DevBuf<uint32_t> real_ptrs;
     DevBuf<uint32_t> v2r;
     DevBuf<uint32_t> masks;
     DevBuf<uint32_t> row_ids;
 };
 
-// build_bvss (R:src/bvss.cpp:19-101) on the GPU from the (permuted) out-view.
-DeviceBvss bvss_build(const DeviceGraph& g);
+// build_bvss (R:src/bvss.cpp:19-101) on the GPU from the (permuted) out-view. With a row
+// range, only arcs into rows [row_lo, row_hi) are packed (the multi-GPU row partition:
+// all n/8 column slice sets, this rank's destination rows; row ids stay global).
+DeviceBvss bvss_build(const DeviceGraph& g, uint32_t row_lo = 0, uint32_t row_hi = 0xFFFFFFFFu);
 
 // Upload a host structure (R:include/blest/bvss.hpp:34-50 public fields), validated.
 DeviceBvss bvss_upload(uint32_t n, uint64_t m, uint32_t num_vss, const uint32_t* real_ptrs,

@@ -17,9 +17,30 @@ using namespace blestgpu;
 struct blest_graph_s {
     DeviceGraph g;
 };
+namespace blestgpu {
+struct PartEngine;
+PartEngine* part_create(const DeviceBvss& b);
+void part_destroy(PartEngine* e);
+void part_range(const PartEngine& e, uint32_t* row_lo, uint32_t* row_hi, uint64_t* w_lo, uint64_t* w_hi);
+uint64_t part_begin(PartEngine& e, uint32_t src);
+void part_pull(PartEngine& e, uint64_t len);
+uint64_t part_sweep(PartEngine& e, uint32_t level, uint32_t* diff_out_dev);
+uint64_t part_enqueue(PartEngine& e, const uint32_t* full_diff_dev, uint64_t* total_bits);
+void part_levels(const PartEngine& e, uint32_t* levels_host);
+struct PartDel {
+    void operator()(PartEngine* e) const { part_destroy(e); }
+};
+}  // namespace blestgpu
+
 struct blest_bvss_s {
     DeviceBvss b;
     std::unique_ptr<BfsEngine> engine;
+    std::unique_ptr<PartEngine, PartDel> part;
+    uint64_t part_len = 0;
+    PartEngine& pe() {
+        if (!part) part.reset(part_create(b));
+        return *part;
+    }
     std::vector<uint64_t> last_phase_ns;
     BfsEngine& eng() {
         if (!engine) engine = std::make_unique<BfsEngine>(b);
@@ -347,6 +368,63 @@ int blest_bvss_build(blest_graph g, blest_bvss* out) {
     auto h = std::make_unique<blest_bvss_s>();
     h->b = bvss_build(g->g);
     *out = h.release();
+    API_END
+}
+
+int blest_bvss_build_rows(blest_graph g, uint32_t row_lo, uint32_t row_hi, blest_bvss* out) {
+    API_BEGIN
+    NEED(g && out, "null argument");
+    NEED((row_lo % 32 == 0 || row_lo >= g->g.n) && (row_hi % 32 == 0 || row_hi >= g->g.n),
+         "row range must be 32-aligned");
+    NEED(row_lo <= row_hi, "empty row range");
+    auto h = std::make_unique<blest_bvss_s>();
+    h->b = bvss_build(g->g, row_lo, row_hi);
+    *out = h.release();
+    API_END
+}
+
+int blest_part_range(blest_bvss b, uint32_t* row_lo, uint32_t* row_hi, uint64_t* word_lo, uint64_t* word_hi) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    part_range(b->pe(), row_lo, row_hi, word_lo, word_hi);
+    API_END
+}
+
+int blest_part_begin(blest_bvss b, uint32_t src, uint64_t* queue_len) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    b->part_len = part_begin(b->pe(), src);
+    if (queue_len) *queue_len = b->part_len;
+    API_END
+}
+
+int blest_part_pull(blest_bvss b) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    part_pull(b->pe(), b->part_len);
+    API_END
+}
+
+int blest_part_sweep(blest_bvss b, uint32_t level, uint32_t* diff_out, uint64_t* discovered) {
+    API_BEGIN
+    NEED(b && diff_out, "null argument");
+    const uint64_t d = part_sweep(b->pe(), level, diff_out);
+    if (discovered) *discovered = d;
+    API_END
+}
+
+int blest_part_enqueue(blest_bvss b, const uint32_t* full_diff, uint64_t* queue_len, uint64_t* total_discovered) {
+    API_BEGIN
+    NEED(b && full_diff, "null argument");
+    b->part_len = part_enqueue(b->pe(), full_diff, total_discovered);
+    if (queue_len) *queue_len = b->part_len;
+    API_END
+}
+
+int blest_part_levels(blest_bvss b, uint32_t* levels_out) {
+    API_BEGIN
+    NEED(b && levels_out, "null argument");
+    part_levels(b->pe(), levels_out);
     API_END
 }
 
