@@ -156,6 +156,12 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
                         vw[c] = cnt[c] ? (VIS[u[c] >> 5] | reinterpret_cast<const uint32_t*>(Fc8)[u[c] >> 5]) : ~0u;
+                    // not visited before: already claimed this level? (F_next at L2; a stale
+                    // miss only costs the atomic) — spares the returned atomic on dense levels
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (!((vw[c] >> (u[c] & 31)) & 1u) && ((ld_l2_u32(Fn + (u[c] >> 5)) >> (u[c] & 31)) & 1u))
+                            vw[c] |= 1u << (u[c] & 31);
                     uint32_t old[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c)

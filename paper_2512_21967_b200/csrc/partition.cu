@@ -57,27 +57,45 @@ __global__ void k_part_begin(uint32_t n, uint32_t row_lo, uint32_t row_hi, uint6
 __global__ void k_part_pull(const unsigned long long* __restrict__ Q, unsigned long long len,
                             const uint32_t* __restrict__ masks, const uint4* __restrict__ rows4,
                             const uint32_t* __restrict__ Vc, uint32_t* Vn, unsigned long long* ctr) {
+    constexpr int B = 4;  // VSSs in flight per warp (as the fused lazy kernel's stage 1)
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t NW = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t pol = evict_first_policy();
     uint32_t reds = 0;
-    for (uint64_t q = gw; q < len; q += NW) {
-        const unsigned long long e = Q[q];
-        const uint64_t v = (uint32_t)e;
-        const uint32_t alpha = (uint32_t)(e >> 32) & 0xFFu;
-        const uint32_t m = ld_stream_u32(masks + 32 * v + lane, pol);
-        const uint4 r = ld_stream_u4(rows4 + 32 * v + lane, pol);
-        const uint32_t x = m & (alpha * 0x01010101u);
-        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+    for (uint64_t p0 = gw; p0 < len; p0 += NW * B) {
+        unsigned long long e = ~0ull;
+        if (lane < B && p0 + lane * NW < len) e = Q[p0 + lane * NW];
+        uint32_t m[B], alpha[B];
+        uint4 r[B];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (!((x >> (8 * c)) & 0xFFu)) continue;
-            const uint32_t bit = 1u << (u[c] & 31);
-            if (Vc[u[c] >> 5] & bit) continue;               // visited before this level
-            if (ld_l2_u32(Vn + (u[c] >> 5)) & bit) continue;  // already marked this level
-            atomicOr(Vn + (u[c] >> 5), bit);
-            ++reds;
+        for (int j = 0; j < B; ++j) {
+            const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
+            alpha[j] = ej == ~0ull ? 0u : (uint32_t)(ej >> 32) & 0xFFu;
+            m[j] = 0;
+            r[j] = make_uint4(0, 0, 0, 0);
+            if (ej != ~0ull) {
+                const uint64_t v = (uint32_t)ej;
+                m[j] = ld_stream_u32(masks + 32 * v + lane, pol);
+                r[j] = ld_stream_u4(rows4 + 32 * v + lane, pol);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const uint32_t x = m[j] & (alpha[j] * 0x01010101u);
+            const uint32_t u[4] = {r[j].x, r[j].y, r[j].z, r[j].w};
+            uint32_t vw[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) vw[c] = ((x >> (8 * c)) & 0xFFu) ? Vc[u[c] >> 5] : ~0u;  // before ℓ?
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (!((vw[c] >> (u[c] & 31)) & 1u)) vw[c] = ld_l2_u32(Vn + (u[c] >> 5));  // marked at ℓ?
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (!((vw[c] >> (u[c] & 31)) & 1u)) {
+                    atomicOr(Vn + (u[c] >> 5), 1u << (u[c] & 31));
+                    ++reds;
+                }
         }
     }
     reds = warp_sum(reds);
@@ -171,7 +189,7 @@ uint64_t part_begin(PartEngine& e, uint32_t src) {
 
 void part_pull(PartEngine& e, uint64_t len) {
     if (!len) return;
-    k_part_pull<<<grid_for(len * 32, 256), 256, 0, stream()>>>(e.Q.p, len, e.b.masks.p,
+    k_part_pull<<<grid_for(len * 8, 256), 256, 0, stream()>>>(e.Q.p, len, e.b.masks.p,
                                                                reinterpret_cast<const uint4*>(e.b.row_ids.p), e.Vc.p,
                                                                e.Vn.p, e.ctr.p);
     CK(cudaGetLastError());
