@@ -34,13 +34,14 @@
 
 #include "bfs.cuh"
 #include "bfs_device.cuh"
+#include "hubs.cuh"
 
 namespace blestgpu {
 
 extern std::atomic<uint64_t> g_launches;
 
 void* eager_kernel(int pull, int threads);       // bfs_eager.cu
-void* lazy_kernel(int pull, int threads);        // bfs_lazy.cu (register-pipelined variant)
+void* lazy_kernel(int pull, int threads, bool hubs);  // bfs_lazy.cu
 void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
 size_t lazy_tma_smem(int consumers);
 
@@ -54,7 +55,8 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     const uint64_t levels_bound = (uint64_t)b.n + 2;
     trace_cap_ = (uint32_t)std::min<uint64_t>(levels_bound, 1u << 20);
     levels_.alloc(b.n ? b.n : 1);
-    bits_.alloc(4 * (words_ ? words_ : 1));
+    wstride_ = (words_ + 3) / 4 * 4;  // 16-byte aligned bitmaps (stage 2 reads uint4)
+    bits_.alloc(4 * (wstride_ ? wstride_ : 4));
     q_.alloc(3 * (uint64_t)(b.num_vss ? b.num_vss : 1));
     ctl_.alloc(8);
     agg_.alloc(4096);
@@ -64,9 +66,6 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     bar_.alloc(4);  // count, pad, {payload | generation}
     trace_.alloc(8ull * trace_cap_);
     tstamp_.alloc(3ull * trace_cap_);
-    // hub prefix staged in shared memory on dense lazy levels (opt-in): at most what one
-    // SM's shared memory holds, whole 16-byte granules inside the V_curr array
-    hub_words_max_ = (uint32_t)std::min<uint64_t>(words_ / 4 * 4, 56u * 1024);
     CK(cudaMallocHost(&pinned_, 8 * sizeof(unsigned long long)));
 }
 
@@ -80,50 +79,53 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     const bool lazy_tma = opt.mode == Mode::Lazy && (opt.lazy_tma || (var_env && std::string(var_env) == "tma"));
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
     const int consumers = nc_env ? atoi(nc_env) : 8;
+    const char* hub_env = getenv("BLEST_HUBS");
+    const bool hubs = opt.mode == Mode::Lazy && !lazy_tma && opt.hubs && !(hub_env && atoi(hub_env) == 0) &&
+                      b_.n < kHubFlag;
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
         kern = eager_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
     else
         kern = lazy_tma ? lazy_tma_kernel(opt.pull == Pull::Mma ? 1 : 0, consumers)
-                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
+                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads, hubs);
     size_t dyn = 0;
+    uint32_t hub_smem_bits = 0;
     if (lazy_tma) {
         dyn = lazy_tma_smem(consumers);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    }
-    int per_sm = 0;
-    if (!lazy_tma) {  // small shared footprint: give the rest of the SM's 256 KB to L1
-        const char* co = getenv("BLEST_CARVEOUT");
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, co ? atoi(co) : 0));
-    }
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dyn));
-    if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
-    // Lazy: give each co-resident CTA an equal share of the SM's shared memory for the
-    // hub prefix (minus the static part), rounded down to 16-byte granules.
-    uint32_t hub_words = 0;
-    const char* hub_env = getenv("BLEST_HUB_CACHE");
-    const bool hub_cache = opt.hub_cache || (hub_env && atoi(hub_env) != 0);
-    if (opt.mode == Mode::Lazy && !lazy_tma && hub_cache && hub_words_max_) {
+    } else if (hubs) {
+        // Hub snapshot: each co-resident CTA gets an equal share of the SM's shared memory
+        // (minus static parts and a 16 KB L1 floor), in whole 128 B lines of hub bits.
         cudaFuncAttributes fa;
         CK(cudaFuncGetAttributes(&fa, kern));
         int dev = 0, smem_sm = 0, smem_blk = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
         CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const int64_t share = std::min<int64_t>(smem_sm / per_sm - 1024, smem_blk) - (int64_t)fa.sharedSizeBytes;
-        if (share >= 1024) {
-            hub_words = (uint32_t)std::min<uint64_t>(hub_words_max_, (uint64_t)share / 4 / 4 * 4);
-            dyn = (size_t)hub_words * 4;
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-            int check = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&check, kern, threads, dyn));
-            if (check < per_sm) {  // keep the register-limited occupancy
-                hub_words = 0;
-                dyn = 0;
-            }
+        const int64_t ctas_sm = std::max(1, 1024 / threads);
+        int64_t share = std::min<int64_t>((smem_sm - 16 * 1024) / ctas_sm, smem_blk) - fa.sharedSizeBytes - 1024;
+        if (const char* cap = getenv("BLEST_HUB_BYTES")) share = std::min<int64_t>(share, atoll(cap));
+        const uint64_t cap_bits = share > 0 ? (uint64_t)share / 128 * 1024 : 0;
+        if (!hub_built_ || hub_cap_bits_ != cap_bits) {
+            hub_view_build(b_, (uint32_t)cap_bits, (uint32_t)(32 * wstride_), hub_);
+            vnx_.alloc(wstride_ + (uint64_t)hub_.bits / 32 + 4);  // V_next | HN
+            hub_built_ = true;
+            hub_cap_bits_ = cap_bits;
         }
+        hub_smem_bits = (uint32_t)std::min<uint64_t>(cap_bits, hub_.bits);
+        dyn = hub_smem_bits / 8;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        const int pct = (int)std::min<int64_t>(
+            100, (100 * ctas_sm * ((int64_t)dyn + fa.sharedSizeBytes + 1024) + smem_sm - 1) / smem_sm);
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    } else {  // small shared footprint: give the rest of the SM's 256 KB to L1
+        const char* co = getenv("BLEST_CARVEOUT");
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, co ? atoi(co) : 0));
     }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dyn));
+    if (per_sm < 1) throw CudaError("BFS kernel cannot be resident");
     uint32_t ctas = (uint32_t)per_sm * (uint32_t)num_sms();
     if (opt.grid_ctas && opt.grid_ctas < ctas) ctas = opt.grid_ctas;
     if (ctas > agg_.count) ctas = (uint32_t)agg_.count;
@@ -136,9 +138,9 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.rows4 = reinterpret_cast<const uint4*>(b_.row_ids.p);
     p.L = levels_.p;
     p.B0 = bits_.p;
-    p.B1 = bits_.p + words_;
-    p.B2 = bits_.p + 2 * words_;
-    p.B3 = bits_.p + 3 * words_;
+    p.B1 = bits_.p + wstride_;
+    p.B2 = bits_.p + 2 * wstride_;
+    p.B3 = bits_.p + 3 * wstride_;
     const uint64_t qcap = b_.num_vss ? b_.num_vss : 1;
     p.Q0 = q_.p;
     p.Q1 = q_.p + qcap;
@@ -154,14 +156,23 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
-    p.hub_words = hub_words;
+    if (hubs) {
+        p.B1 = vnx_.p;
+        p.rows4h = reinterpret_cast<const uint4*>(hub_.rows.p);
+        p.HN = vnx_.p + wstride_;
+        p.hub_base = (uint32_t)(32 * wstride_);
+        p.hub_rows = hub_.hub_rows.p;
+        p.hub_of = hub_.hub_of.p;
+        p.hub_bits = hub_.bits;
+        p.hub_smem_bits = hub_smem_bits;
+    }
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
+    if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);
     cudaStream_t st = stream();
     CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
     void* args[] = {&p};
     CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, dyn, st));
-    last_hub_words_ = hub_words;
     g_launches.fetch_add(1);
     last_ctas_ = ctas;
     last_threads_ = threads;

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "bvss.cuh"
+#include "hubs.cuh"
 
 namespace blestgpu {
 
@@ -19,7 +20,7 @@ struct EngineOptions {
     uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
-    bool hub_cache = false;   // lazy (plain variant): stage the hub prefix of V_curr in smem
+    bool hubs = true;         // lazy: hub view + shared-memory visited snapshot (hubs.cuh)
     bool lazy_tma = false;    // lazy: TMA producer/consumer pipeline (measured slower on C2)
 };
 
@@ -56,12 +57,11 @@ public:
     uint32_t last_grid_ctas() const { return last_ctas_; }
     uint32_t last_threads() const { return last_threads_; }
     uint32_t last_src() const { return last_src_; }
-    uint32_t last_hub_words() const { return last_hub_words_; }
     const DeviceBvss& bvss() const { return b_; }
 
 private:
     const DeviceBvss& b_;
-    uint64_t words_ = 0;
+    uint64_t words_ = 0, wstride_ = 0;
     uint32_t trace_cap_ = 0;
     DevBuf<uint32_t> levels_;
     DevBuf<uint32_t> bits_;              // 3 * words_
@@ -70,7 +70,10 @@ private:
     DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA VSS counts
     DevBuf<unsigned long long> aggS_;    // lazy stage-2 per-CTA slice-set counts
     DevBuf<unsigned long long> sl_;      // lazy queue: active slice sets
-    uint32_t hub_words_max_ = 0, last_hub_words_ = 0;
+    HubView hub_;                        // lazy: built on the first hub-view launch
+    DevBuf<uint32_t> vnx_;               // lazy hub view: V_next extended by the hubs' bits (HN)
+    bool hub_built_ = false;
+    uint64_t hub_cap_bits_ = 0;
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
     DevBuf<unsigned long long> tstamp_;  // trace_cap_ * 3

@@ -40,9 +40,18 @@ struct Params {
     uint32_t src;
     uint32_t cap;
     uint32_t num_warps;
-    uint32_t hub_words;      // lazy: V_curr words [0, hub_words) staged in shared memory on
-                             // dense levels (0 = off; the L1 then caches the hub prefix)
-    uint64_t dense_min;      // queue length from which a level stages the hub prefix
+    uint64_t dense_min;  // queue length from which a level counts as dense (eager re-checks,
+                         // lazy hub snapshot)
+    // lazy hub view (hubs.cuh): engine row ids (hub_base + h for hubs), the hubs'
+    // cumulative V_next (HN = V_next + hub_base / 32), h -> row, row -> h; hub_smem_bits
+    // of HN are staged in shared memory on dense levels
+    const uint4* __restrict__ rows4h;
+    uint32_t* HN;
+    const uint32_t* __restrict__ hub_rows;
+    const uint32_t* __restrict__ hub_of;
+    uint32_t hub_base;
+    uint32_t hub_bits;
+    uint32_t hub_smem_bits;
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
 };
 
@@ -65,6 +74,83 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Fire-and-forget OR (REDG): the lazy scheme's "relaxed atomic" (R:src/bfs_engine.cpp:287-288).
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v));
+}
+
+// Visited-test building blocks, written in PTX so each is a handful of SASS instructions
+// with no branch: 32-bit word index, one IMAD.WIDE for the address, SHF.L.W for the bit.
+// cand_word: the bitmap word holding bit x if `m & sel` (the lane's pull hit column x),
+// else all ones (= "visited", nothing more to do). Plain ld.global: L1-cached.
+__device__ __forceinline__ uint32_t cand_word(const uint32_t* base, uint32_t x, uint32_t m, uint32_t sel) {
+    uint32_t v;
+    asm("{\n\t.reg .pred q;\n\t.reg .b64 a;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %3, %4;\n\tsetp.ne.u32 q, t, 0;\n\t"
+        "shr.u32 t, %2, 5;\n\tmul.wide.u32 a, t, 4;\n\tadd.s64 a, a, %1;\n\t"
+        "mov.b32 %0, -1;\n\t@q ld.global.u32 %0, [a];\n\t}"
+        : "=r"(v)
+        : "l"(base), "r"(x), "r"(m), "r"(sel));
+    return v;
+}
+// recheck_word: v if it has bit x, else the word re-read at L2 (ld.relaxed.gpu).
+__device__ __forceinline__ uint32_t recheck_word(const uint32_t* base, uint32_t x, uint32_t v) {
+    uint32_t r;
+    asm("{\n\t.reg .pred q;\n\t.reg .b64 a;\n\t.reg .b32 t, b;\n\t"
+        "shf.l.wrap.b32 b, 0, 1, %2;\n\tand.b32 t, %3, b;\n\tsetp.eq.u32 q, t, 0;\n\t"
+        "shr.u32 t, %2, 5;\n\tmul.wide.u32 a, t, 4;\n\tadd.s64 a, a, %1;\n\t"
+        "mov.b32 %0, %3;\n\t@q ld.relaxed.gpu.global.u32 %0, [a];\n\t}"
+        : "=r"(r)
+        : "l"(base), "r"(x), "r"(v));
+    return r;
+}
+// red_if_clear: if v lacks bit x, RED it into the bitmap; returns 1 if a RED was issued.
+__device__ __forceinline__ uint32_t red_if_clear(uint32_t* base, uint32_t x, uint32_t v) {
+    uint32_t issued;
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .b64 a;\n\t.reg .b32 t, b;\n\t"
+        "shf.l.wrap.b32 b, 0, 1, %2;\n\tand.b32 t, %3, b;\n\tsetp.eq.u32 q, t, 0;\n\t"
+        "shr.u32 t, %2, 5;\n\tmul.wide.u32 a, t, 4;\n\tadd.s64 a, a, %1;\n\t"
+        "@q red.relaxed.gpu.global.or.b32 [a], b;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+        : "=r"(issued)
+        : "l"(base), "r"(x), "r"(v));
+    return issued;
+}
+
+// atom_if_clear: if v lacks bit x, atomicOr the bit into the bitmap and return the old
+// word (its bit clear ⇒ this lane set it); else return all ones.
+__device__ __forceinline__ uint32_t atom_if_clear(uint32_t* base, uint32_t x, uint32_t v) {
+    uint32_t r;
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .b64 a;\n\t.reg .b32 t, b;\n\t"
+        "shf.l.wrap.b32 b, 0, 1, %2;\n\tand.b32 t, %3, b;\n\tsetp.eq.u32 q, t, 0;\n\t"
+        "shr.u32 t, %2, 5;\n\tmul.wide.u32 a, t, 4;\n\tadd.s64 a, a, %1;\n\t"
+        "mov.b32 %0, -1;\n\t@q atom.relaxed.gpu.global.or.b32 %0, [a], b;\n\t}"
+        : "=r"(r)
+        : "l"(base), "r"(x), "r"(v));
+    return r;
+}
+
+// Hub view (hubs.cuh): an engine row id X >= hub_base is hub h = X - hub_base, whose
+// V_next bit lives at the same index X of the extended V_next (HN directly follows V_next),
+// so the re-check and RED phases need no hub logic. cand_word_h: the visited-before test
+// reads the hub's bit from the shared-memory snapshot when h < hub_n, else returns 0 ("not
+// known visited", settled by the V_next re-check); rows read V_curr as in cand_word.
+__device__ __forceinline__ uint32_t cand_word_h(const uint32_t* base, uint32_t hub_s, uint32_t hub_base,
+                                                uint32_t hub_n, uint32_t x, uint32_t m, uint32_t sel) {
+    uint32_t v;
+    asm("{\n\t.reg .pred q, qg, qs;\n\t.reg .b64 a;\n\t.reg .b32 t, h;\n\t"
+        "and.b32 t, %6, %7;\n\tsetp.ne.u32 q, t, 0;\n\t"
+        "sub.u32 h, %5, %3;\n\tsetp.lt.u32 qg, %5, %3;\n\tsetp.lt.and.u32 qs, h, %4, q;\n\t"
+        "and.pred qg, qg, q;\n\t"
+        "selp.b32 %0, 0, -1, q;\n\t"
+        "shr.u32 t, %5, 5;\n\tmul.wide.u32 a, t, 4;\n\tadd.s64 a, a, %1;\n\t@qg ld.global.u32 %0, [a];\n\t"
+        "shr.u32 t, h, 3;\n\tand.b32 t, t, 0x1ffffffc;\n\tadd.u32 t, t, %2;\n\t@qs ld.shared.u32 %0, [t];\n\t}"
+        : "=r"(v)
+        : "l"(base), "r"(hub_s), "r"(hub_base), "r"(hub_n), "r"(x), "r"(m), "r"(sel));
+    return v;
+}
+
+// Predicated RED (no branch / reconvergence point per call site).
+__device__ __forceinline__ void red_or_if(bool pred, uint32_t* p, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(p),
+        "r"(v), "r"((uint32_t)pred));
 }
 
 template <int MODE>
@@ -283,111 +369,159 @@ __device__ __forceinline__ uint32_t find_set(const Params& p, uint32_t S, uint64
 }
 
 
-// Lazy stage 2 (R:src/bfs_engine.cpp:296-338), shared by both lazy kernels: each CTA owns a
-// contiguous chunk of the ⌈n/32⌉ words. Pass A: diff = V_next & ~V_curr, V_curr |= diff,
-// diff words kept in Fd (α of the next level, like the reference's in-place F_curr,
-// :310-311), levels written with one coalesced 128 B store per changed word, set/VSS
-// counts reduced. The CTA publishes both counts (tagged with the level, so no reset) and
-// sums its predecessors'; pass B writes its SL entries (set | first position << 32).
-// The last CTA stores the grid totals (the next level's T, S) in ctl[0], ctl[1].
+// Lazy stage 2 (R:src/bfs_engine.cpp:296-338), shared by both lazy kernels. The ⌈n/32⌉
+// words are cut into chunks of 4·THREADS (one uint4 of words per thread) and each CTA owns
+// a contiguous run of chunks. Pass A, per chunk: diff = V_next & ~V_curr, V_curr = V_next,
+// diff words stored in Fd (α of the next level, like the reference's in-place F_curr,
+// :310-311), levels written with one coalesced 128 B store per changed word, and the
+// thread's active slice sets / their VSSs counted (real_ptrs lookups only for nonzero diff
+// bytes). The CTA publishes both counts (tagged with the level, so no reset) and sums its
+// predecessors'; pass B writes its SL entries (set | first position << 32) in ascending
+// order, reusing the diff words held in registers when the CTA owns one chunk. The last
+// CTA stores the grid totals (the next level's T, S) in ctl[0], ctl[1].
+template <int THREADS>
+__device__ __forceinline__ void s2_counts(const Params& p, uint64_t w0, const uint32_t (&d)[4],
+                                          unsigned long long& nv, unsigned long long& ns) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if ((d[k] >> (8 * b)) & 0xFFu) {
+                const uint64_t ss = 4 * (w0 + k) + b;
+                const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
+                nv += c;
+                ns += c != 0;  // sets without VSSs push nothing
+            }
+        }
+    }
+}
+
+template <int THREADS>
+__device__ __forceinline__ void s2_load(const Params& p, const uint32_t* src, uint64_t w0, uint32_t (&d)[4], bool cg) {
+    if (w0 + 4 <= p.words) {
+        const uint4 v = cg ? __ldcg(reinterpret_cast<const uint4*>(src + w0)) : *reinterpret_cast<const uint4*>(src + w0);
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[k] = (w0 + k < p.words) ? (cg ? __ldcg(src + w0 + k) : src[w0 + k]) : 0u;
+    }
+}
+
 template <int THREADS>
 __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
                                             uint32_t (&ctr)[4]) {
     constexpr unsigned long long kTagMask = (1ull << 40) - 1;
+    constexpr uint64_t CH = 4ull * THREADS;
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
     uint32_t* Fd = p.B2;
-        const uint64_t per = ((p.words + gridDim.x - 1) / gridDim.x + THREADS - 1) / THREADS * THREADS;
-        const uint64_t w0 = (uint64_t)blockIdx.x * per;
-        const uint64_t w1 = min(w0 + per, p.words);
-        unsigned long long my_vss = 0, my_sets = 0;
-        // pass A
-        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-            const uint64_t w = wb + threadIdx.x;
-            uint32_t diff = 0;
-            if (w < w1) {
-                const uint32_t nx = Vn[w];
-                diff = nx & ~Vc[w];
-                Fd[w] = diff;
-                if (diff) Vc[w] = nx;
-                for (uint32_t d = diff; d;) {
-                    const int bsel = (__ffs(d) - 1) >> 3;
-                    d &= ~(0xFFu << (8 * bsel));
-                    const uint64_t ss = 4 * w + bsel;
-                    const uint32_t c = p.rp[ss + 1] - p.rp[ss];
-                    my_vss += c;
-                    my_sets += c != 0;  // sets without VSSs push nothing
-                }
-            }
-            ctr[0] += __popc(diff);
-            const uint64_t wwarp = wb + 32 * warp;
-            unsigned ball = __ballot_sync(0xffffffffu, diff != 0);
-            while (ball) {
-                const int k = __ffs(ball) - 1;
-                ball &= ball - 1;
-                const uint32_t dk = __shfl_sync(0xffffffffu, diff, k);
-                if ((dk >> lane) & 1u) p.L[32 * (wwarp + k) + lane] = level;
-            }
-        }
-        unsigned long long cta_vss = 0, cta_sets = 0;
-        block_excl_scan(sm, my_vss, &cta_vss);
-        block_excl_scan(sm, my_sets, &cta_sets);
-        if (threadIdx.x == 0) {
-            const unsigned long long tag = (unsigned long long)level << 40;
-            p.aggS[blockIdx.x] = tag | cta_sets;
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag | cta_vss)
-                         : "memory");
-        }
-        unsigned long long bv = 0, bs = 0;
-        for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
-            unsigned long long x;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
-            } while ((x >> 40) != level);
-            bv += x & kTagMask;
-            bs += ld_relaxed_gpu_u64(p.aggS + c) & kTagMask;
-        }
-        unsigned long long run_vss = 0, run_sets = 0;
-        block_excl_scan(sm, bv, &run_vss);
-        block_excl_scan(sm, bs, &run_sets);
-        if (threadIdx.x == 0) {
-            ctr[3] += (uint32_t)cta_vss;
-            if (blockIdx.x == gridDim.x - 1) {  // grid totals: the next level's T, S
-                p.ctl[0] = run_vss + cta_vss;
-                p.ctl[1] = run_sets + cta_sets;
-            }
-        }
-        // pass B: SL entries of the chunk's active sets, ascending
-        for (uint64_t wb = w0; wb < w1; wb += THREADS) {
-            const uint64_t w = wb + threadIdx.x;
-            const uint32_t diff = (w < w1) ? Fd[w] : 0u;
-            unsigned long long nv = 0, ns = 0;
-            uint32_t cnts[4];
+    const uint64_t chunks = (p.words + CH - 1) / CH;
+    const uint64_t k0 = (uint64_t)blockIdx.x * chunks / gridDim.x, k1 = (uint64_t)(blockIdx.x + 1) * chunks / gridDim.x;
+    const bool single = k1 - k0 <= 1;
+    uint32_t keep[4] = {0, 0, 0, 0};  // diff words of the CTA's only chunk
+    unsigned long long my_vss = 0, my_sets = 0;
+    // pass A
+    for (uint64_t ch = k0; ch < k1; ++ch) {
+        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
+        uint32_t nx[4], cu[4], d[4];
+        s2_load<THREADS>(p, Vn, w0, nx, true);  // REDs landed in L2
+        s2_load<THREADS>(p, Vc, w0, cu, false);
+        bool any = false;
 #pragma unroll
-            for (int bsel = 0; bsel < 4; ++bsel) {
-                cnts[bsel] = 0;
-                if ((diff >> (8 * bsel)) & 0xFFu) {
-                    const uint64_t ss = 4 * w + bsel;
-                    cnts[bsel] = p.rp[ss + 1] - p.rp[ss];
-                    nv += cnts[bsel];
-                    ns += cnts[bsel] != 0;
-                }
-            }
-            unsigned long long it_v = 0, it_s = 0;
-            unsigned long long pv = run_vss + block_excl_scan(sm, nv, &it_v);
-            unsigned long long ps = run_sets + block_excl_scan(sm, ns, &it_s);
-#pragma unroll
-            for (int bsel = 0; bsel < 4; ++bsel) {
-                if (cnts[bsel]) {
-                    p.SL[ps++] = (pv << 32) | (4 * w + bsel);
-                    pv += cnts[bsel];
-                }
-            }
-            run_vss += it_v;
-            run_sets += it_s;
+        for (int k = 0; k < 4; ++k) {
+            d[k] = nx[k] & ~cu[k];
+            any |= d[k] != 0;
+            ctr[0] += __popc(d[k]);
+            keep[k] = d[k];
         }
+        if (w0 + 4 <= p.words) {
+            *reinterpret_cast<uint4*>(Fd + w0) = make_uint4(d[0], d[1], d[2], d[3]);
+            if (any) *reinterpret_cast<uint4*>(Vc + w0) = make_uint4(nx[0], nx[1], nx[2], nx[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (w0 + k < p.words) {
+                    Fd[w0 + k] = d[k];
+                    if (d[k]) Vc[w0 + k] = nx[k];
+                }
+        }
+        s2_counts<THREADS>(p, w0, d, my_vss, my_sets);
+        // levels: one coalesced 128 B store per changed word (lane = bit)
+        unsigned ball = __ballot_sync(0xffffffffu, any);
+        const uint64_t wwarp = ch * CH + 128ull * warp;
+        while (ball) {
+            const int src = __ffs(ball) - 1;
+            ball &= ball - 1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t dk = __shfl_sync(0xffffffffu, d[k], src);
+                if ((dk >> lane) & 1u) p.L[32 * (wwarp + 4 * src + k) + lane] = level;
+            }
+        }
+    }
+    unsigned long long cta_vss = 0, cta_sets = 0;
+    block_excl_scan(sm, my_vss, &cta_vss);
+    block_excl_scan(sm, my_sets, &cta_sets);
+    if (threadIdx.x == 0) {
+        const unsigned long long tag = (unsigned long long)level << 40;
+        p.aggS[blockIdx.x] = tag | cta_sets;
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag | cta_vss) : "memory");
+    }
+    unsigned long long bv = 0, bs = 0;
+    for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
+        unsigned long long x;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
+        } while ((x >> 40) != level);
+        bv += x & kTagMask;
+        bs += ld_relaxed_gpu_u64(p.aggS + c) & kTagMask;
+    }
+    unsigned long long run_vss = 0, run_sets = 0;
+    block_excl_scan(sm, bv, &run_vss);
+    block_excl_scan(sm, bs, &run_sets);
+    if (threadIdx.x == 0) {
+        ctr[3] += (uint32_t)cta_vss;
+        if (blockIdx.x == gridDim.x - 1) {  // grid totals: the next level's T, S
+            p.ctl[0] = run_vss + cta_vss;
+            p.ctl[1] = run_sets + cta_sets;
+        }
+    }
+    // pass B: SL entries of the CTA's active sets, ascending
+    for (uint64_t ch = k0; ch < k1; ++ch) {
+        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
+        uint32_t d[4];
+        if (single) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) d[k] = keep[k];
+        } else {
+            s2_load<THREADS>(p, Fd, w0, d, false);
+        }
+        unsigned long long nv = 0, ns = 0;
+        s2_counts<THREADS>(p, w0, d, nv, ns);
+        unsigned long long it_v = 0, it_s = 0;
+        unsigned long long pv = run_vss + block_excl_scan(sm, nv, &it_v);
+        unsigned long long ps = run_sets + block_excl_scan(sm, ns, &it_s);
+        if (ns) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if ((d[k] >> (8 * b)) & 0xFFu) {
+                        const uint64_t ss = 4 * (w0 + k) + b;
+                        const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
+                        if (c) {
+                            p.SL[ps++] = (pv << 32) | ss;
+                            pv += c;
+                        }
+                    }
+                }
+            }
+        }
+        run_vss += it_v;
+        run_sets += it_s;
+    }
 }
 
 }  // namespace bfsdev

@@ -8,15 +8,16 @@
 // Queue entries are 64-bit: low = VSS id, high = slice set (saves virtual_to_real, :192);
 // α is the set's byte of F_curr (frontier_byte :148-151), loaded beside the mask/row loads.
 //
-// Sink (:198-211): the reference's levels[u] test becomes "VIS | F_curr" — two plain
-// 4-byte bitmap loads (2 × n/8 bytes, L1/L2-resident, unlike the 4n-byte level array):
-// VIS holds every discovery up to level ℓ-2 (level ℓ-1's discoveries are F_curr, frozen;
-// they are ORed into VIS during this level's pull with a RED per dequeued VSS — adding
-// bits that F_curr already has, so concurrent readers' union never changes). A clear test elects the discoverer with
-// one atomicOr into F_next (old bit clear), which stores levels[u] = ℓ; the first bit of
-// a slice set in F_next this level (old byte zero, :204-205) pushes the set's VSS range. Pushes gather in a per-warp shared
-// buffer; a flush reserves queue space with ONE atomicAdd per buffer (warp-aggregated
-// reservation) and expands [real_ptrs[s], real_ptrs[s+1]).
+// Sink (:198-211): the reference's levels[u] test becomes one visited bitmap VIS
+// (n/8 bytes, L1/L2-resident, unlike the 4n-byte level array) holding every discovery of
+// the previous levels (and, lagging, of this one). A clear VIS bit goes to an atomicOr on
+// F_next, which ELECTS the discoverer (old bit clear) and, through its old byte, tells
+// whether u is its slice set's first discovery this level (:204-205) ⇒ push the set's VSS
+// range; the discoverer stores levels[u] = ℓ and REDs u into VIS. The tests of a warp's
+// whole batch (kBatch VSSs × 4 columns per lane) run as phases — all VIS loads, then (dense
+// levels) the F_next re-checks at L2, then the atomics — so each phase costs one latency.
+// Pushes gather in a per-warp shared buffer; a flush reserves queue space with ONE
+// atomicAdd per buffer (warp-aggregated reservation) and expands [real_ptrs[s], real_ptrs[s+1]).
 //
 // Frontier bitmaps are triple-buffered: level ℓ reads F[ℓ%3], ORs into F[(ℓ+1)%3], and
 // zeroes the bytes of F[(ℓ+2)%3] that level ℓ-1 read (set ids fetched from queue ℓ-1 at
@@ -31,6 +32,12 @@ namespace blestgpu {
 
 namespace {
 using namespace bfsdev;
+
+// Row id of flat candidate k (VSS k / 4, column k % 4); constant-folded when unrolled.
+__device__ __forceinline__ uint32_t row_of(const uint4 (&rw)[kBatch], int k) {
+    const uint4& r = rw[k >> 2];
+    return (k & 3) == 0 ? r.x : (k & 3) == 1 ? r.y : (k & 3) == 2 ? r.z : r.w;
+}
 
 template <int PULL, int THREADS>
 #ifndef BLEST_EAGER_MINB
@@ -62,7 +69,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
         p.B0[w] = 0;
         p.B1[w] = seed;  // F[1] = F_curr of level 1
         p.B2[w] = 0;
-        VIS[w] = 0;  // the source is in F_curr of level 1
+        VIS[w] = seed;  // every discovery so far (the source)
     }
     {
         const unsigned long long aux = (unsigned long long)sset << 32;
@@ -115,6 +122,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
         const unsigned long long* Qz = qsel(k2);
         const uint32_t zss = (gtid < prev_len) ? (uint32_t)(Qz[gtid] >> 32) : 0xFFFFFFFFu;
 
+        const bool recheck = len >= p.dense_min;  // sparse levels: straight to the atomic
         // ---- pull over the queue (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
             unsigned long long e_next = kNoEntry;
@@ -127,10 +135,6 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                     if (pos < len) e_next = Qc[pos];
                 }
                 const uint32_t alpha_l = (e != kNoEntry) ? Fc8[e >> 32] : 0u;  // frontier_byte
-                if (e != kNoEntry) {  // fold level ℓ-1's discoveries of this set into VIS
-                    const uint32_t ss = (uint32_t)(e >> 32);
-                    red_or(VIS + (ss >> 2), alpha_l << (8 * (ss & 3)));
-                }
                 uint32_t mk[kBatch];
                 uint4 rw[kBatch];
                 unsigned long long ej[kBatch];
@@ -145,40 +149,60 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                         rw[j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
                     }
                 }
+                // Sink (R:src/bfs_engine.cpp:198-211) in batch-wide phases, each phase's
+                // memory operations in flight together (branch-free PTX blocks): (A) VIS word
+                // (L1) of every column with a nonzero pull; (B) dense levels only: F_next at
+                // L2 for the rest (claimed this level already?) to spare the atomic; (C)
+                // atomicOr on F_next elects the discoverer (old bit clear) and its old byte
+                // says whether it is the set's first discovery this level (push, :204-205);
+                // (D) the discoverer stores the level and REDs its VIS bit.
+                uint32_t vw[4 * kBatch];
+                if (PULL == 0) {
 #pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    if (ej[j] == kNoEntry) continue;  // warp-uniform
-                    const uint32_t alpha = __shfl_sync(0xffffffffu, alpha_l, j);
-                    uint32_t cnt[4];
-                    column_counts<PULL>(mk[j], alpha, cnt);
-                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-                    uint32_t vw[4];
+                    for (int j = 0; j < kBatch; ++j) {  // absent entries: no candidates
+                        const uint32_t a = ej[j] != kNoEntry ? __shfl_sync(0xffffffffu, alpha_l, j) : 0u;
+                        const uint32_t m = mk[j] & (a * 0x01010101u);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        vw[c] = cnt[c] ? (VIS[u[c] >> 5] | reinterpret_cast<const uint32_t*>(Fc8)[u[c] >> 5]) : ~0u;
-                    // not visited before: already claimed this level? (F_next at L2; a stale
-                    // miss only costs the atomic) — spares the returned atomic on dense levels
+                        for (int c = 0; c < 4; ++c) vw[4 * j + c] = cand_word(VIS, row_of(rw, 4 * j + c), m, 0xFFu << (8 * c));
+                    }
+                } else {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (!((vw[c] >> (u[c] & 31)) & 1u) && ((ld_l2_u32(Fn + (u[c] >> 5)) >> (u[c] & 31)) & 1u))
-                            vw[c] |= 1u << (u[c] & 31);
-                    uint32_t old[4];
+                    for (int j = 0; j < kBatch; ++j) {
+                        uint32_t cnt[4] = {0, 0, 0, 0};
+                        const uint32_t a = __shfl_sync(0xffffffffu, alpha_l, j);
+                        if (ej[j] != kNoEntry) column_counts<PULL>(mk[j], a, cnt);  // warp-uniform
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        old[c] = ((vw[c] >> (u[c] & 31)) & 1u) ? ~0u : atomicOr(Fn + (u[c] >> 5), 1u << (u[c] & 31));
+                        for (int c = 0; c < 4; ++c) vw[4 * j + c] = cand_word(VIS, row_of(rw, 4 * j + c), cnt[c], ~0u);
+                    }
+                }
+                if (recheck) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        bool push = false;
-                        if (!((vw[c] >> (u[c] & 31)) & 1u)) {
-                            ++ctr[1];
-                            if (!((old[c] >> (u[c] & 31)) & 1u)) {  // this lane discovered u
-                                p.L[u[c]] = level;
-                                ++ctr[0];
-                                push = ((old[c] >> (8 * ((u[c] >> 3) & 3))) & 0xFFu) == 0;
-                            }
-                        }
-                        push_column(p, push, (unsigned long long)(u[c] >> 3) << 32 | (u[c] >> 3), pbuf, pcount,
-                                    Qn, qlen_next, ctr[3], ctr[1]);
+                    for (int k = 0; k < 4 * kBatch; ++k) vw[k] = recheck_word(Fn, row_of(rw, k), vw[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < 4 * kBatch; ++k) {
+                    const uint32_t x = row_of(rw, k);
+                    ctr[1] += ((vw[k] >> (x & 31)) & 1u) ^ 1u;  // full atomics (R:src/bfs_engine.cpp:203)
+                    vw[k] = atom_if_clear(Fn, x, vw[k]);
+                }
+                uint32_t disc = 0;
+#pragma unroll
+                for (int k = 0; k < 4 * kBatch; ++k) {
+                    const uint32_t x = row_of(rw, k);
+                    if (!((vw[k] >> (x & 31)) & 1u)) {  // rare: this lane discovered x
+                        disc |= 1u << k;
+                        p.L[x] = level;
+                        red_or(VIS + (x >> 5), 1u << (x & 31));
+                    }
+                }
+                ctr[0] += __popc(disc);
+                if (__any_sync(0xffffffffu, disc != 0)) {
+#pragma unroll
+                    for (int k = 0; k < 4 * kBatch; ++k) {
+                        const uint32_t x = row_of(rw, k);
+                        const bool push = ((disc >> k) & 1u) && ((vw[k] >> (8 * ((x >> 3) & 3))) & 0xFFu) == 0;
+                        push_column(p, push, (unsigned long long)(x >> 3) << 32 | (x >> 3), pbuf, pcount, Qn,
+                                    qlen_next, ctr[3], ctr[1]);
                     }
                 }
             }

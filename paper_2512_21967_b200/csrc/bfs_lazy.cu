@@ -7,7 +7,9 @@
 // enqueued it). Per VSS: one coalesced 128 B mask line and four 128 B row-id lines
 // (streaming loads), AND with α, and for every nonzero column the visited test: V_curr
 // (frozen during the stage, L1-cached) and, if clear, V_next at L2; only then a
-// fire-and-forget RED sets the V_next bit (legal per SURVEY §8(a) pitfall 7).
+// fire-and-forget RED sets the V_next bit (legal per SURVEY §8(a) pitfall 7). The tests
+// of a warp's whole batch run as three phases (all V_curr loads, then the V_next
+// re-checks, then the REDs), so a batch pays each latency once, not once per VSS.
 //
 // Stage 2 (word sweep, :296-338) is lazy_stage2 (bfs_device.cuh): balanced, no contended
 // atomics; it emits the next queue as the ascending list SL of active slice sets (set id,
@@ -24,14 +26,87 @@ namespace {
 using namespace bfsdev;
 
 
-template <int PULL, int THREADS>
 #ifndef BLEST_MINB
 #define BLEST_MINB 1
 #endif
+// Visited tests of one batch (kBatch VSSs × 4 columns per lane) in three batch-wide phases,
+// each phase's memory operations in flight together (one latency per phase, not one per
+// VSS): (A) for every column with a nonzero pull, visited before this level? — V_curr
+// (frozen, L1); (B) for the rest, marked this level already? — V_next at L2 (skipped with
+// xflags bit 2); (C) a fire-and-forget RED for what is still clear. Branch-free PTX blocks
+// (bfs_device.cuh). rows(j) / mask(j) give the lane's row ids and mask word of VSS j; the
+// row ids are re-read per phase, so a shared-memory source keeps them out of registers.
+// Returns the number of REDs issued.
+// HUBS: the rows come from the hub view (hubs.cuh); hub candidates are tested against the
+// hubs' visited snapshot in shared memory (hub_s / hub_n), then against HN — the extension
+// of V_next — like any row, and a hub's first discoverers also mark its row in V_next.
+template <int PULL, bool HUBS, typename Rows, typename Mask>
+__device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t* Vc, uint32_t* Vn, unsigned long long e,
+                                                Rows rows, Mask mask, uint32_t hub_s, uint32_t hub_n) {
+    uint32_t vw[4 * kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
+        const uint4 r = rows(j);
+        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+        uint32_t m[4], sel[4];
+        if (PULL == 0) {  // absent entries: α = 0, no candidates
+            const uint32_t a = ej != kNoEntry ? (uint32_t)(ej >> 32) & 0xFFu : 0u;
+            const uint32_t mm = mask(j) & (a * 0x01010101u);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                m[c] = mm;
+                sel[c] = 0xFFu << (8 * c);
+            }
+        } else {
+            uint32_t cnt[4] = {0, 0, 0, 0};
+            if (ej != kNoEntry)  // warp-uniform (mma.sync needs the whole warp)
+                column_counts<PULL>(mask(j), (uint32_t)(ej >> 32) & 0xFFu, cnt);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                m[c] = cnt[c];
+                sel[c] = ~0u;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            vw[4 * j + c] = HUBS ? cand_word_h(Vc, hub_s, p.hub_base, hub_n, u[c], m[c], sel[c])
+                                 : cand_word(Vc, u[c], m[c], sel[c]);
+    }
+    if (!(p.xflags & 2)) {
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const uint4 r = rows(j);
+            const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                vw[4 * j + c] = recheck_word(Vn, u[c], vw[4 * j + c]);
+        }
+    }
+    uint32_t reds = 0;
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        const uint4 r = rows(j);
+        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t did = red_if_clear(Vn, u[c], vw[4 * j + c]);
+            reds += did;
+            if (HUBS && did && u[c] >= p.hub_base) {  // rare: a hub's first discoverers
+                const uint32_t row = p.hub_rows[u[c] - p.hub_base];
+                red_or(Vn + (row >> 5), 1u << (row & 31));
+            }
+        }
+    }
+    return reds;
+}
+
+template <int PULL, int THREADS, bool HUBS>
 __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)) k_bfs_lazy(Params p) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
-    extern __shared__ uint32_t hub[];  // optional: V_curr bits of the hub prefix
+    extern __shared__ uint4 dyn_smem[];  // HUBS: the hubs' visited snapshot
+    const uint32_t hub_s = static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem));
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
@@ -45,6 +120,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
     uint32_t* Fd = p.B2;
+    const uint4* __restrict__ rows4 = HUBS ? p.rows4h : p.rows4;
 
     // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
     const uint32_t src = p.src;
@@ -57,6 +133,11 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         Vc[w] = seed;
         Vn[w] = seed;
         Fd[w] = seed;  // α of the source's set for level 1
+    }
+    if (HUBS) {  // the source is visited: its hub bit too
+        const uint32_t hs = p.hub_of[src];
+        for (uint64_t w = gtid; w < (uint64_t)p.hub_bits / 32; w += gthreads)
+            p.HN[w] = (hs != 0xFFFFFFFFu && w == hs >> 5) ? 1u << (hs & 31) : 0u;
     }
     if (threadIdx.x == 0) {
         p.agg[blockIdx.x] = 0;
@@ -120,68 +201,43 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                 }
             }
         }
-        grid_barrier(p.bar, gen);
-        const bool hubs = p.hub_words && len >= p.dense_min;
-        const uint32_t hub_n = hubs ? 32u * p.hub_words : 0u;
-        if (hubs) {
-            const uint4* src4 = reinterpret_cast<const uint4*>(Vc);
-            uint4* dst4 = reinterpret_cast<uint4*>(hub);
-            for (uint32_t i = threadIdx.x; i < p.hub_words / 4; i += THREADS) dst4[i] = src4[i];
-            __syncthreads();
+        // dense level: stage the hubs' visited snapshot (HN is quiescent outside stage 1)
+        const uint32_t hub_n = (HUBS && len >= p.dense_min) ? p.hub_smem_bits : 0u;
+        if (HUBS && hub_n) {
+            const uint4* src4 = reinterpret_cast<const uint4*>(p.HN);
+            for (uint32_t i = threadIdx.x; i < hub_n / 128; i += THREADS) dyn_smem[i] = __ldcg(src4 + i);
         }
+        grid_barrier(p.bar, gen);  // its block barrier also publishes the snapshot
 
         // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
-            // queue entries of the next batch are fetched while this batch is processed
-            unsigned long long e_next = kNoEntry;
-            if (lane < kBatch && gw + (uint64_t)lane * NW < len) e_next = Qc[gw + (uint64_t)lane * NW];
-            for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
+            // Position walk: round-robin over all warps like the reference (p ≡ warp mod
+            // #warps, :190). (A CTA-contiguous walk, for L1 sharing among an SM's warps,
+            // measured no better.)
+            const uint64_t qstride = NW, q0 = gw, qend = len;
+            const uint64_t step = qstride * kBatch;
+            auto qload = [&](uint64_t base) -> unsigned long long {
+                const uint64_t pos = base + (uint64_t)lane * qstride;
+                return (lane < kBatch && pos < qend) ? Qc[pos] : kNoEntry;
+            };
+            // Register batches: kBatch VSSs' mask words and row ids loaded together (streaming
+            // loads), queue entries of the next batch fetched while this batch is processed.
+            unsigned long long e_next = qload(q0);
+            for (uint64_t p0 = q0; p0 < qend; p0 += step) {
                 const unsigned long long e = e_next;
-                e_next = kNoEntry;
-                if (lane < kBatch) {
-                    const uint64_t pos = p0 + (uint64_t)NW * kBatch + (uint64_t)lane * NW;
-                    if (pos < len) e_next = Qc[pos];
-                }
+                e_next = qload(p0 + step);
                 uint32_t mk[kBatch];
                 uint4 rw[kBatch];
-                unsigned long long ej[kBatch];
 #pragma unroll
                 for (int j = 0; j < kBatch; ++j) {
-                    ej[j] = __shfl_sync(0xffffffffu, e, j);
-                    mk[j] = 0;
-                    rw[j] = make_uint4(0, 0, 0, 0);
-                    if (ej[j] != kNoEntry) {
-                        const uint64_t v = (uint32_t)ej[j];
-                        mk[j] = ld_stream_u32(p.masks + 32 * v + lane, pol);
-                        rw[j] = ld_stream_u4(p.rows4 + 32 * v + lane, pol);
-                    }
+                    const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
+                    const bool ok = ej != kNoEntry;
+                    const uint64_t v = ok ? (uint32_t)ej : 0u;
+                    mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
+                    rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
                 }
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    if (ej[j] == kNoEntry) continue;  // warp-uniform
-                    uint32_t cnt[4];
-                    column_counts<PULL>(mk[j], (uint32_t)((ej[j] >> 32) & 0xFFu), cnt);
-                    const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-                    // visited before this level? (V_curr, frozen; hub prefix from smem)
-                    uint32_t vw[4];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        bool need = cnt[c] != 0;
-                        if (need && u[c] < hub_n) need = !((hub[u[c] >> 5] >> (u[c] & 31)) & 1u);
-                        vw[c] = (need && !(p.xflags & 1)) ? Vc[u[c] >> 5] : (need ? 0u : ~0u);
-                    }
-                    // not yet: already marked this level by anyone? (V_next at L2)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (!((vw[c] >> (u[c] & 31)) & 1u) && !(p.xflags & 2)) vw[c] = ld_l2_u32(Vn + (u[c] >> 5));
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        if (!((vw[c] >> (u[c] & 31)) & 1u)) {
-                            red_or(Vn + (u[c] >> 5), 1u << (u[c] & 31));
-                            ++ctr[2];
-                        }
-                    }
-                }
+                ctr[2] += check_batch<PULL, HUBS>(
+                    p, Vc, Vn, e, [&](int j) { return rw[j]; }, [&](int j) { return mk[j]; }, hub_s, hub_n);
             }
         }
         level_barrier(p, sm, gen, level, ctr, 1);
@@ -194,20 +250,19 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
 
 }  // namespace
 
-void* lazy_kernel(int pull, int threads) {
-    if (pull == 1) {
-        switch (threads) {
-            case 256: return (void*)k_bfs_lazy<1, 256>;
-            case 512: return (void*)k_bfs_lazy<1, 512>;
-            case 1024: return (void*)k_bfs_lazy<1, 1024>;
-        }
-    } else {
-        switch (threads) {
-            case 256: return (void*)k_bfs_lazy<0, 256>;
-            case 512: return (void*)k_bfs_lazy<0, 512>;
-            case 1024: return (void*)k_bfs_lazy<0, 1024>;
-        }
+void* lazy_kernel(int pull, int threads, bool hubs) {
+#define BLEST_LAZY_CASES(PULL, HUBS)                         \
+    switch (threads) {                                       \
+        case 256: return (void*)k_bfs_lazy<PULL, 256, HUBS>;   \
+        case 512: return (void*)k_bfs_lazy<PULL, 512, HUBS>;   \
+        case 1024: return (void*)k_bfs_lazy<PULL, 1024, HUBS>; \
     }
+    if (pull == 1) {
+        if (hubs) { BLEST_LAZY_CASES(1, true) } else { BLEST_LAZY_CASES(1, false) }
+    } else {
+        if (hubs) { BLEST_LAZY_CASES(0, true) } else { BLEST_LAZY_CASES(0, false) }
+    }
+#undef BLEST_LAZY_CASES
     throw InvalidArgument("threads per CTA must be 256, 512 or 1024");
 }
 

@@ -243,3 +243,37 @@ def test_auto_pipeline_maps_levels_back(oracle):
             r = B.run_auto_prebuilt(b, plan, int(src), cfg)
             assert np.array_equal(r.bfs.levels, oracle.reference_bfs(csr, int(src))[0]), strat
             assert r.bfs.source == int(src)
+
+
+@pytest.mark.parametrize("env", [
+    {},
+    {"BLEST_XFLAGS": "2"},                 # lazy: no V_next re-check before the RED
+    {"BLEST_DENSE_MIN": "1"},              # eager: F_next re-check on every level
+    {"BLEST_DENSE_MIN": "1000000000"},     # eager: never (straight to the atomic)
+])
+def test_engine_phase_variants(oracle, monkeypatch, env):
+    """The batch-wide visited-test phases and their switches change only how the tests are
+    answered: levels and every deterministic counter equal the reference engine's, for both
+    engines and pulls, on undirected and directed graphs, including a hub source."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for directed in (False, True):
+        s, d = oracle.gen_rmat(14, 16, 5)
+        n = 1 << 14
+        csr = oracle.from_edges(n, s, d, directed=directed)
+        g = B.Graph.from_csr(n, csr.offsets, csr.targets, directed=directed)
+        b = B.build_bvss(g)
+        ob = oracle.build_bvss(csr)
+        deg = np.diff(csr.offsets.astype(np.int64))
+        hub_src = int(np.argmax(deg))
+        srcs = [hub_src] + [int(x) for x in oracle.pick_sources(csr, 3, 9)]
+        for src in srcs:
+            want = oracle.reference_bfs(csr, src)[0]
+            for mode in ("eager", "lazy"):
+                o_eng = oracle.run_engine(ob, src, mode == "lazy")
+                for pull in ("popc", "mma"):
+                    res, cnt = run(b, src, mode, pull)
+                    assert np.array_equal(res.levels, want), (env, directed, src, mode, pull)
+                    assert cnt.vss_dequeues == o_eng.counters["vss_dequeues"]
+                    assert cnt.queue_pushes == o_eng.counters["queue_pushes"]
+                    assert np.array_equal(trace_cols(cnt)[:, [1, 3, 4]], o_eng.trace[:, [1, 3, 7]])
