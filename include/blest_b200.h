@@ -170,6 +170,13 @@ typedef struct {
  * equivalents: BLEST_EINVAL (src >= n), BLEST_ERUNTIME (level cap exceeded). */
 int blest_bfs(blest_bvss b, uint32_t src, const blest_engine_config* cfg, uint32_t* levels_out,
               blest_counters* counters, blest_level_trace* trace_out, uint32_t trace_cap);
+/* Many sources back to back (the CLI's / acceptance loop over sources, R:tools/blest.cpp:283,
+ * R:tests/acceptance_main.cpp:246-263, as one call): source k's levels land in
+ * levels_out + k*n (host, may be NULL), counters in counters[k] (may be NULL). The device
+ * pipelines it: the level array of source k is copied to the host while source k+1 runs.
+ * Errors as blest_bfs (checked for every source before any work). */
+int blest_bfs_batch(blest_bvss b, const uint32_t* srcs, uint32_t count, const blest_engine_config* cfg,
+                    uint32_t* levels_out, blest_counters* counters);
 /* Asynchronous split of blest_bfs for stream-ordered timing: launch enqueues the fused
  * kernel (init + all levels) on the library stream; finish waits and reads back. */
 int blest_bfs_launch(blest_bvss b, uint32_t src, const blest_engine_config* cfg);

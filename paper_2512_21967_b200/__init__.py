@@ -8,5 +8,5 @@ from .api import (  # noqa: F401
     build_bvss, bvss_stats, choose_mode, classify_social_like, compression_ratio, device_info,
     engine_mode_from_string, init_state, jaccard_with_windows, make_permutation,
     ordering_strategy_from_string, prepare, random_order, rcm, relabel_permutation, run_auto,
-    run_auto_prebuilt, run_eager, run_lazy, select_plan, update_divergence)
+    run_auto_prebuilt, run_batch, run_eager, run_lazy, select_plan, update_divergence)
 from ._lib import BlestCudaError, BlestLogicError, LIB_PATH  # noqa: F401

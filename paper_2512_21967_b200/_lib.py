@@ -114,6 +114,7 @@ SIGNATURES = {
     "blest_bfs": (i32, [vp, u32, P(EngineConfigT), vp, P(CountersT), vp, u32]),
     "blest_bfs_launch": (i32, [vp, u32, P(EngineConfigT)]),
     "blest_bfs_finish": (i32, [vp, vp, P(CountersT), vp, u32]),
+    "blest_bfs_batch": (i32, [vp, vp, u32, P(EngineConfigT), vp, vp]),
     "blest_bfs_levels_device": (i32, [vp, P(vp)]),
     "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),

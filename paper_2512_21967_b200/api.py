@@ -579,6 +579,28 @@ def run_lazy(b: Bvss, src: int, cfg: EngineConfig | None = None):
     return _run(b, src, cfg or EngineConfig(), EngineMode.Lazy)
 
 
+def run_batch(b: Bvss, srcs, mode: EngineMode, cfg: EngineConfig | None = None, out=None):
+    """Many sources back to back through blest_bfs_batch (device-pipelined: source k's level
+    array is copied to the host while source k+1 runs). Returns (levels [k, n] uint32 —
+    `out` if given, e.g. pinned memory — and one EngineCounters per source, trace rows
+    omitted). Same results as calling run_eager / run_lazy per source."""
+    cfg = cfg or EngineConfig()
+    if mode == EngineMode.Auto:
+        raise ValueError("run_batch needs a resolved mode (eager or lazy)")
+    srcs = np.ascontiguousarray(srcs, np.uint32)
+    k = len(srcs)
+    lv = out if out is not None else np.zeros((k, max(b.n, 1)), np.uint32)
+    ctr = (L.CountersT * max(k, 1))()
+    cs = _cfg_struct(cfg, mode)
+    ptr = lv.data_ptr() if hasattr(lv, "data_ptr") else lv.ctypes.data
+    L.check(L.lib().blest_bfs_batch(b.handle, _ptr(srcs) if k else None, k, C.byref(cs), C.c_void_p(ptr),
+                                    C.cast(ctr, C.c_void_p)))
+    cnts = [EngineCounters(c.mma_calls, c.full_atomics, c.relaxed_atomics, c.queue_pushes, c.vss_dequeues,
+                           c.brs_baseline_mma_calls, c.levels_processed, [], bool(c.trace_truncated))
+            for c in list(ctr)[:k]]
+    return lv, cnts
+
+
 @dataclass
 class AutoConfig:
     engine: EngineConfig = field(default_factory=EngineConfig)

@@ -34,19 +34,49 @@
 
 #include "bfs.cuh"
 #include "bfs_device.cuh"
-#include "hubs.cuh"
 
 namespace blestgpu {
 
 extern std::atomic<uint64_t> g_launches;
 
 void* eager_kernel(int pull, int threads);       // bfs_eager.cu
-void* lazy_kernel(int pull, int threads, bool hubs);  // bfs_lazy.cu
+void* lazy_kernel(int pull, int threads);        // bfs_lazy.cu
 void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
 size_t lazy_tma_smem(int consumers);
 
 namespace {
 using namespace bfsdev;
+
+// Per-source summary of a finished launch (run_batch): [0] iterations, [1] max level,
+// [2] runaway, [3] Σ queue, [4] Σ discovered, [5] Σ full, [6] Σ relaxed, [7] Σ pushes.
+__global__ void k_summarise(const unsigned long long* __restrict__ ctl, const unsigned long long* __restrict__ trace,
+                            uint32_t trace_cap, unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long acc[5];
+    if (threadIdx.x < 5) acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t rows = ctl[4] < trace_cap ? ctl[4] : trace_cap;
+    unsigned long long q = 0, d = 0, f = 0, r = 0, pu = 0;
+    for (uint64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+        const unsigned long long* t = trace + 8 * i;
+        q += t[1];
+        d += t[3];
+        f += t[4];
+        r += t[6];
+        pu += t[7];
+    }
+    atomicAdd(&acc[0], q);
+    atomicAdd(&acc[1], d);
+    atomicAdd(&acc[2], f);
+    atomicAdd(&acc[3], r);
+    atomicAdd(&acc[4], pu);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = ctl[4];
+        out[1] = ctl[5];
+        out[2] = ctl[6];
+        for (int i = 0; i < 5; ++i) out[3 + i] = acc[i];
+    }
+}
 
 }  // namespace
 
@@ -79,46 +109,17 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     const bool lazy_tma = opt.mode == Mode::Lazy && (opt.lazy_tma || (var_env && std::string(var_env) == "tma"));
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
     const int consumers = nc_env ? atoi(nc_env) : 8;
-    const char* hub_env = getenv("BLEST_HUBS");
-    const bool hubs = opt.mode == Mode::Lazy && !lazy_tma && opt.hubs && !(hub_env && atoi(hub_env) == 0) &&
-                      b_.n < kHubFlag;
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
         kern = eager_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
     else
         kern = lazy_tma ? lazy_tma_kernel(opt.pull == Pull::Mma ? 1 : 0, consumers)
-                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads, hubs);
+                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
     size_t dyn = 0;
-    uint32_t hub_smem_bits = 0;
     if (lazy_tma) {
         dyn = lazy_tma_smem(consumers);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    } else if (hubs) {
-        // Hub snapshot: each co-resident CTA gets an equal share of the SM's shared memory
-        // (minus static parts and a 16 KB L1 floor), in whole 128 B lines of hub bits.
-        cudaFuncAttributes fa;
-        CK(cudaFuncGetAttributes(&fa, kern));
-        int dev = 0, smem_sm = 0, smem_blk = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-        CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const int64_t ctas_sm = std::max(1, 1024 / threads);
-        int64_t share = std::min<int64_t>((smem_sm - 16 * 1024) / ctas_sm, smem_blk) - fa.sharedSizeBytes - 1024;
-        if (const char* cap = getenv("BLEST_HUB_BYTES")) share = std::min<int64_t>(share, atoll(cap));
-        const uint64_t cap_bits = share > 0 ? (uint64_t)share / 128 * 1024 : 0;
-        if (!hub_built_ || hub_cap_bits_ != cap_bits) {
-            hub_view_build(b_, (uint32_t)cap_bits, (uint32_t)(32 * wstride_), hub_);
-            vnx_.alloc(wstride_ + (uint64_t)hub_.bits / 32 + 4);  // V_next | HN
-            hub_built_ = true;
-            hub_cap_bits_ = cap_bits;
-        }
-        hub_smem_bits = (uint32_t)std::min<uint64_t>(cap_bits, hub_.bits);
-        dyn = hub_smem_bits / 8;
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        const int pct = (int)std::min<int64_t>(
-            100, (100 * ctas_sm * ((int64_t)dyn + fa.sharedSizeBytes + 1024) + smem_sm - 1) / smem_sm);
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     } else {  // small shared footprint: give the rest of the SM's 256 KB to L1
         const char* co = getenv("BLEST_CARVEOUT");
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, co ? atoi(co) : 0));
@@ -136,7 +137,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.rp = b_.real_ptrs.p;
     p.masks = b_.masks.p;
     p.rows4 = reinterpret_cast<const uint4*>(b_.row_ids.p);
-    p.L = levels_.p;
+    p.L = level_target_ ? level_target_ : levels_.p;
     p.B0 = bits_.p;
     p.B1 = bits_.p + wstride_;
     p.B2 = bits_.p + 2 * wstride_;
@@ -156,16 +157,6 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
-    if (hubs) {
-        p.B1 = vnx_.p;
-        p.rows4h = reinterpret_cast<const uint4*>(hub_.rows.p);
-        p.HN = vnx_.p + wstride_;
-        p.hub_base = (uint32_t)(32 * wstride_);
-        p.hub_rows = hub_.hub_rows.p;
-        p.hub_of = hub_.hub_of.p;
-        p.hub_bits = hub_.bits;
-        p.hub_smem_bits = hub_smem_bits;
-    }
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
     if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);
@@ -179,6 +170,77 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     last_src_ = src;
     last_mode_ = opt.mode;
     launched_ = true;
+}
+
+std::vector<BfsOutcome> BfsEngine::run_batch(const uint32_t* srcs, uint32_t count, const EngineOptions& opt,
+                                             uint32_t* levels_host) {
+    for (uint32_t k = 0; k < count; ++k)
+        if (srcs[k] >= b_.n) throw InvalidArgument("bfs source out of range");
+    std::vector<BfsOutcome> outs(count);
+    if (!count) return outs;
+    if (!levels2_.p) levels2_.alloc(b_.n ? b_.n : 1);
+    DevBuf<unsigned long long> summ(8ull * count);
+    cudaStream_t st = stream(), cp = nullptr;
+    cudaEvent_t kern_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+    CK(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&kern_done[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
+    }
+    uint32_t* bufs[2] = {levels_.p, levels2_.p};
+    try {
+        for (uint32_t k = 0; k < count; ++k) {
+            const int s = k & 1;
+            if (k >= 2) CK(cudaStreamWaitEvent(st, copy_done[s], 0));  // buffer s free again
+            level_target_ = bufs[s];
+            launch(srcs[k], opt);
+            level_target_ = nullptr;
+            k_summarise<<<1, 256, 0, st>>>(ctl_.p, trace_.p, trace_cap_, summ.p + 8ull * k);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(kern_done[s], st));
+            if (levels_host && b_.n) {
+                CK(cudaStreamWaitEvent(cp, kern_done[s], 0));
+                CK(cudaMemcpyAsync(levels_host + (uint64_t)k * b_.n, bufs[s], (size_t)b_.n * 4,
+                                   cudaMemcpyDeviceToHost, cp));
+            }
+            CK(cudaEventRecord(copy_done[s], cp));
+        }
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamSynchronize(cp));
+    } catch (...) {
+        level_target_ = nullptr;
+        cudaStreamSynchronize(cp);
+        cudaStreamDestroy(cp);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(kern_done[i]);
+            cudaEventDestroy(copy_done[i]);
+        }
+        throw;
+    }
+    CK(cudaStreamDestroy(cp));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventDestroy(kern_done[i]));
+        CK(cudaEventDestroy(copy_done[i]));
+    }
+    std::vector<unsigned long long> h(8ull * count);
+    CK(cudaMemcpy(h.data(), summ.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t k = 0; k < count; ++k) {
+        const unsigned long long* x = h.data() + 8ull * k;
+        if (x[2])
+            throw RuntimeError("BFS ran past the level safety cap at level " + std::to_string(x[0] + 1) +
+                               " — engine invariant broken");
+        BfsOutcome& o = outs[k];
+        o.iterations = (uint32_t)x[0];
+        o.max_level = (uint32_t)x[1];
+        o.visited = 1 + x[4];
+        o.trace_truncated = x[0] > trace_cap_;
+        o.sum_queue = x[3];
+        o.sum_full = x[5];
+        o.sum_relaxed = x[6];
+        o.sum_pushes = x[7];
+    }
+    launched_ = false;
+    return outs;
 }
 
 BfsOutcome BfsEngine::finish(uint32_t* levels_host) {
@@ -201,6 +263,10 @@ BfsOutcome BfsEngine::finish(uint32_t* levels_host) {
     for (uint32_t i = 0; i < rows; ++i) {
         TraceRow& r = out.trace[i];
         visited += r.discovered;
+        out.sum_queue += r.queue_size;
+        out.sum_full += r.full_atomics;
+        out.sum_relaxed += r.relaxed_atomics;
+        out.sum_pushes += r.queue_pushes;
         r.frontier_population = (i == 0) ? 1 : out.trace[i - 1].discovered;
         r.stage1_full_atomics = (last_mode_ == Mode::Eager) ? r.full_atomics : 0;
     }

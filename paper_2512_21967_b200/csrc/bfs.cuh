@@ -4,9 +4,9 @@
 #pragma once
 
 #include <vector>
+#include <cstdint>
 
 #include "bvss.cuh"
-#include "hubs.cuh"
 
 namespace blestgpu {
 
@@ -20,7 +20,6 @@ struct EngineOptions {
     uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
-    bool hubs = true;         // lazy: hub view + shared-memory visited snapshot (hubs.cuh)
     bool lazy_tma = false;    // lazy: TMA producer/consumer pipeline (measured slower on C2)
 };
 
@@ -37,6 +36,8 @@ struct BfsOutcome {
     bool trace_truncated = false;
     std::vector<TraceRow> trace;
     std::vector<uint64_t> phase_ns;  // per level: start, stage-1 end (lazy), level end
+    // totals over the levels (run_batch fills these instead of `trace`)
+    uint64_t sum_queue = 0, sum_full = 0, sum_relaxed = 0, sum_pushes = 0;
 };
 
 // Per-structure device workspace; sized once, reused across sources.
@@ -52,6 +53,12 @@ public:
     // Wait for the last launch, read back trace/counters, check status (throws
     // RuntimeError past the level cap). Copies levels to host when levels_host != null.
     BfsOutcome finish(uint32_t* levels_host);
+    // BFS from each of `count` sources back to back, pipelined: source k's level array is
+    // copied to levels_host + k·n (when non-null) on a copy stream while source k+1 runs
+    // (two device level buffers); each kernel's trace is folded on the device into a
+    // per-source summary. Returns per-source outcomes without per-level rows (trace empty).
+    std::vector<BfsOutcome> run_batch(const uint32_t* srcs, uint32_t count, const EngineOptions& opt,
+                                      uint32_t* levels_host);
     const uint32_t* levels_device() const { return levels_.p; }
     uint32_t trace_capacity() const { return trace_cap_; }
     uint32_t last_grid_ctas() const { return last_ctas_; }
@@ -64,16 +71,14 @@ private:
     uint64_t words_ = 0, wstride_ = 0;
     uint32_t trace_cap_ = 0;
     DevBuf<uint32_t> levels_;
+    DevBuf<uint32_t> levels2_;           // run_batch: second level buffer
+    uint32_t* level_target_ = nullptr;   // launch(): level array written (null = levels_)
     DevBuf<uint32_t> bits_;              // 3 * words_
     DevBuf<unsigned long long> q_;       // 3 * max(num_vss, 1) entries
     DevBuf<unsigned long long> ctl_;     // qlen[4], result[4]
     DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA VSS counts
     DevBuf<unsigned long long> aggS_;    // lazy stage-2 per-CTA slice-set counts
     DevBuf<unsigned long long> sl_;      // lazy queue: active slice sets
-    HubView hub_;                        // lazy: built on the first hub-view launch
-    DevBuf<uint32_t> vnx_;               // lazy hub view: V_next extended by the hubs' bits (HN)
-    bool hub_built_ = false;
-    uint64_t hub_cap_bits_ = 0;
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
     DevBuf<unsigned long long> tstamp_;  // trace_cap_ * 3

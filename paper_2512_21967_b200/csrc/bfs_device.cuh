@@ -40,18 +40,7 @@ struct Params {
     uint32_t src;
     uint32_t cap;
     uint32_t num_warps;
-    uint64_t dense_min;  // queue length from which a level counts as dense (eager re-checks,
-                         // lazy hub snapshot)
-    // lazy hub view (hubs.cuh): engine row ids (hub_base + h for hubs), the hubs'
-    // cumulative V_next (HN = V_next + hub_base / 32), h -> row, row -> h; hub_smem_bits
-    // of HN are staged in shared memory on dense levels
-    const uint4* __restrict__ rows4h;
-    uint32_t* HN;
-    const uint32_t* __restrict__ hub_rows;
-    const uint32_t* __restrict__ hub_of;
-    uint32_t hub_base;
-    uint32_t hub_bits;
-    uint32_t hub_smem_bits;
+    uint64_t dense_min;  // queue length from which a level counts as dense (eager re-checks)
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
 };
 
@@ -124,26 +113,6 @@ __device__ __forceinline__ uint32_t atom_if_clear(uint32_t* base, uint32_t x, ui
         : "=r"(r)
         : "l"(base), "r"(x), "r"(v));
     return r;
-}
-
-// Hub view (hubs.cuh): an engine row id X >= hub_base is hub h = X - hub_base, whose
-// V_next bit lives at the same index X of the extended V_next (HN directly follows V_next),
-// so the re-check and RED phases need no hub logic. cand_word_h: the visited-before test
-// reads the hub's bit from the shared-memory snapshot when h < hub_n, else returns 0 ("not
-// known visited", settled by the V_next re-check); rows read V_curr as in cand_word.
-__device__ __forceinline__ uint32_t cand_word_h(const uint32_t* base, uint32_t hub_s, uint32_t hub_base,
-                                                uint32_t hub_n, uint32_t x, uint32_t m, uint32_t sel) {
-    uint32_t v;
-    asm("{\n\t.reg .pred q, qg, qs;\n\t.reg .b64 a;\n\t.reg .b32 t, h;\n\t"
-        "and.b32 t, %6, %7;\n\tsetp.ne.u32 q, t, 0;\n\t"
-        "sub.u32 h, %5, %3;\n\tsetp.lt.u32 qg, %5, %3;\n\tsetp.lt.and.u32 qs, h, %4, q;\n\t"
-        "and.pred qg, qg, q;\n\t"
-        "selp.b32 %0, 0, -1, q;\n\t"
-        "shr.u32 t, %5, 5;\n\tmul.wide.u32 a, t, 4;\n\tadd.s64 a, a, %1;\n\t@qg ld.global.u32 %0, [a];\n\t"
-        "shr.u32 t, h, 3;\n\tand.b32 t, t, 0x1ffffffc;\n\tadd.u32 t, t, %2;\n\t@qs ld.shared.u32 %0, [t];\n\t}"
-        : "=r"(v)
-        : "l"(base), "r"(hub_s), "r"(hub_base), "r"(hub_n), "r"(x), "r"(m), "r"(sel));
-    return v;
 }
 
 // Predicated RED (no branch / reconvergence point per call site).

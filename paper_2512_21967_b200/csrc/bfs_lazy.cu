@@ -37,12 +37,9 @@ using namespace bfsdev;
 // (bfs_device.cuh). rows(j) / mask(j) give the lane's row ids and mask word of VSS j; the
 // row ids are re-read per phase, so a shared-memory source keeps them out of registers.
 // Returns the number of REDs issued.
-// HUBS: the rows come from the hub view (hubs.cuh); hub candidates are tested against the
-// hubs' visited snapshot in shared memory (hub_s / hub_n), then against HN — the extension
-// of V_next — like any row, and a hub's first discoverers also mark its row in V_next.
-template <int PULL, bool HUBS, typename Rows, typename Mask>
+template <int PULL, typename Rows, typename Mask>
 __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t* Vc, uint32_t* Vn, unsigned long long e,
-                                                Rows rows, Mask mask, uint32_t hub_s, uint32_t hub_n) {
+                                                Rows rows, Mask mask) {
     uint32_t vw[4 * kBatch];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
@@ -70,8 +67,7 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-            vw[4 * j + c] = HUBS ? cand_word_h(Vc, hub_s, p.hub_base, hub_n, u[c], m[c], sel[c])
-                                 : cand_word(Vc, u[c], m[c], sel[c]);
+            vw[4 * j + c] = cand_word(Vc, u[c], m[c], sel[c]);
     }
     if (!(p.xflags & 2)) {
 #pragma unroll
@@ -90,23 +86,16 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
         const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const uint32_t did = red_if_clear(Vn, u[c], vw[4 * j + c]);
-            reds += did;
-            if (HUBS && did && u[c] >= p.hub_base) {  // rare: a hub's first discoverers
-                const uint32_t row = p.hub_rows[u[c] - p.hub_base];
-                red_or(Vn + (row >> 5), 1u << (row & 31));
-            }
+            reds += red_if_clear(Vn, u[c], vw[4 * j + c]);
         }
     }
     return reds;
 }
 
-template <int PULL, int THREADS, bool HUBS>
+template <int PULL, int THREADS>
 __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)) k_bfs_lazy(Params p) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
-    extern __shared__ uint4 dyn_smem[];  // HUBS: the hubs' visited snapshot
-    const uint32_t hub_s = static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem));
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
@@ -120,7 +109,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
     uint32_t* Fd = p.B2;
-    const uint4* __restrict__ rows4 = HUBS ? p.rows4h : p.rows4;
+    const uint4* __restrict__ rows4 = p.rows4;
 
     // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
     const uint32_t src = p.src;
@@ -133,11 +122,6 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         Vc[w] = seed;
         Vn[w] = seed;
         Fd[w] = seed;  // α of the source's set for level 1
-    }
-    if (HUBS) {  // the source is visited: its hub bit too
-        const uint32_t hs = p.hub_of[src];
-        for (uint64_t w = gtid; w < (uint64_t)p.hub_bits / 32; w += gthreads)
-            p.HN[w] = (hs != 0xFFFFFFFFu && w == hs >> 5) ? 1u << (hs & 31) : 0u;
     }
     if (threadIdx.x == 0) {
         p.agg[blockIdx.x] = 0;
@@ -201,13 +185,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                 }
             }
         }
-        // dense level: stage the hubs' visited snapshot (HN is quiescent outside stage 1)
-        const uint32_t hub_n = (HUBS && len >= p.dense_min) ? p.hub_smem_bits : 0u;
-        if (HUBS && hub_n) {
-            const uint4* src4 = reinterpret_cast<const uint4*>(p.HN);
-            for (uint32_t i = threadIdx.x; i < hub_n / 128; i += THREADS) dyn_smem[i] = __ldcg(src4 + i);
-        }
-        grid_barrier(p.bar, gen);  // its block barrier also publishes the snapshot
+        grid_barrier(p.bar, gen);
 
         // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
@@ -236,8 +214,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                     mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
                     rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
                 }
-                ctr[2] += check_batch<PULL, HUBS>(
-                    p, Vc, Vn, e, [&](int j) { return rw[j]; }, [&](int j) { return mk[j]; }, hub_s, hub_n);
+                ctr[2] += check_batch<PULL>(p, Vc, Vn, e, [&](int j) { return rw[j]; }, [&](int j) { return mk[j]; });
             }
         }
         level_barrier(p, sm, gen, level, ctr, 1);
@@ -250,19 +227,20 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
 
 }  // namespace
 
-void* lazy_kernel(int pull, int threads, bool hubs) {
-#define BLEST_LAZY_CASES(PULL, HUBS)                         \
-    switch (threads) {                                       \
-        case 256: return (void*)k_bfs_lazy<PULL, 256, HUBS>;   \
-        case 512: return (void*)k_bfs_lazy<PULL, 512, HUBS>;   \
-        case 1024: return (void*)k_bfs_lazy<PULL, 1024, HUBS>; \
-    }
+void* lazy_kernel(int pull, int threads) {
     if (pull == 1) {
-        if (hubs) { BLEST_LAZY_CASES(1, true) } else { BLEST_LAZY_CASES(1, false) }
+        switch (threads) {
+            case 256: return (void*)k_bfs_lazy<1, 256>;
+            case 512: return (void*)k_bfs_lazy<1, 512>;
+            case 1024: return (void*)k_bfs_lazy<1, 1024>;
+        }
     } else {
-        if (hubs) { BLEST_LAZY_CASES(0, true) } else { BLEST_LAZY_CASES(0, false) }
+        switch (threads) {
+            case 256: return (void*)k_bfs_lazy<0, 256>;
+            case 512: return (void*)k_bfs_lazy<0, 512>;
+            case 1024: return (void*)k_bfs_lazy<0, 1024>;
+        }
     }
-#undef BLEST_LAZY_CASES
     throw InvalidArgument("threads per CTA must be 256, 512 or 1024");
 }
 

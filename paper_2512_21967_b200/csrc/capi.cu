@@ -522,13 +522,7 @@ EngineOptions to_opts(const blest_engine_config* cfg) {
 }
 
 void fill_counters(const BfsOutcome& r, blest_counters* c, blest_level_trace* trace, uint32_t trace_cap) {
-    uint64_t d = 0, pushes = 0, full = 0, relaxed = 0;
-    for (const TraceRow& t : r.trace) {
-        d += t.queue_size;
-        pushes += t.queue_pushes;
-        full += t.full_atomics;
-        relaxed += t.relaxed_atomics;
-    }
+    const uint64_t d = r.sum_queue, pushes = r.sum_pushes, full = r.sum_full, relaxed = r.sum_relaxed;
     if (c) {
         c->vss_dequeues = d;
         c->mma_calls = 2 * d;  // two m8n8k128 tiles per dequeued VSS (SPEC.md MMA exactness)
@@ -584,6 +578,16 @@ int blest_bfs(blest_bvss b, uint32_t src, const blest_engine_config* cfg, uint32
     const BfsOutcome r = b->eng().finish(levels_out);
     b->last_phase_ns = r.phase_ns;
     fill_counters(r, counters, trace, trace_cap);
+    API_END
+}
+
+int blest_bfs_batch(blest_bvss b, const uint32_t* srcs, uint32_t count, const blest_engine_config* cfg,
+                    uint32_t* levels_out, blest_counters* counters) {
+    API_BEGIN
+    NEED(b && (srcs || !count), "null argument");
+    const std::vector<BfsOutcome> r = b->eng().run_batch(srcs, count, to_opts(cfg), levels_out);
+    if (counters)
+        for (uint32_t k = 0; k < count; ++k) fill_counters(r[k], counters + k, nullptr, 0);
     API_END
 }
 

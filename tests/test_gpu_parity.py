@@ -277,3 +277,23 @@ def test_engine_phase_variants(oracle, monkeypatch, env):
                     assert cnt.vss_dequeues == o_eng.counters["vss_dequeues"]
                     assert cnt.queue_pushes == o_eng.counters["queue_pushes"]
                     assert np.array_equal(trace_cols(cnt)[:, [1, 3, 4]], o_eng.trace[:, [1, 3, 7]])
+
+
+def test_run_batch_pipelined(oracle):
+    """blest_bfs_batch (pipelined level copies) equals per-source blest_bfs: levels bit-exact
+    with the oracle and every counter equal, both engines; a bad source fails before any work."""
+    g = B.Graph.generate_rmat(15, 16, 3)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    b = B.build_bvss(g)
+    srcs = g.pick_sources(5, 4)
+    want, _ = oracle.reference_bfs_many(csr, srcs)
+    for mode, fn in ((B.EngineMode.Eager, B.run_eager), (B.EngineMode.Lazy, B.run_lazy)):
+        lv, cnts = B.run_batch(b, srcs, mode)
+        assert np.array_equal(lv, want)
+        for k, s in enumerate(srcs):
+            _, c1 = fn(b, int(s))
+            assert (cnts[k].vss_dequeues, cnts[k].queue_pushes, cnts[k].levels_processed) == \
+                (c1.vss_dequeues, c1.queue_pushes, c1.levels_processed)
+    with pytest.raises(ValueError):
+        B.run_batch(b, [0, g.num_vertices()], B.EngineMode.Lazy)

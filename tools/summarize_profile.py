@@ -100,7 +100,18 @@ def main():
         res["launch_list"] = launches(lp)
     fp = os.path.join(ROOT, "gpurun_out", f"full_{cfg}.ncu-rep")
     if os.path.exists(fp):
-        res["full_capture"] = full(fp)
+        res["full_capture"] = fc = full(fp)
+        k = fc.get("kernel") or ""
+        if "k_bfs_" in k and fc.get("dram_bytes_total"):
+            # bench.py's roofline.traffic: DRAM bytes of one BFS launch (read + write)
+            engine = "lazy" if "lazy" in k else "eager"
+            full_name = subprocess.run(["ncu", "-i", fp, "--page", "raw", "--csv"], capture_output=True,
+                                       text=True).stdout
+            pull = "mma" if "<1," in full_name or "(int)1," in full_name else "popc"
+            with open(os.path.join(ROOT, "profiles", f"traffic_{cfg}.json"), "w") as f:
+                json.dump(dict(config=cfg, engine=engine, pull=pull, kernel=k,
+                               dram_bytes_per_launch=int(fc["dram_bytes_total"]),
+                               source=f"ncu --set full capture gpurun_out/full_{cfg}.ncu-rep ({tag})"), f, indent=1)
     with open(os.path.join(ROOT, "profiles", f"{tag}_{cfg}_ncu_summary.json"), "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1)[:3000])
