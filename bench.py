@@ -305,6 +305,8 @@ def main():
     if world > 1:
         dist.barrier()
     launches = lib.blest_kernel_launches() - launches0
+    g_ctas, g_thr = C.c_uint32(), C.c_uint32()
+    L.check(lib.blest_bfs_last_geometry(b.handle, C.byref(g_ctas), C.byref(g_thr)))
     L.check(lib.blest_bfs_finish(b.handle, None, C.byref(ctr), None, 0))
     t = np.array([ev[k].elapsed_time(ev[k + 1]) / 1e3 for k in range(len(mine))])
     E = np.array([c["E"] for c in census], np.float64)
@@ -374,7 +376,7 @@ def main():
                           formula="648 D + 4 P + 4 n + 4 V + k (n/8) L (SURVEY 8(d))"),
             cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
             clocks=clk.summary(),
-            detail=dict(hm_gteps_rank0=round(hm, 4), mean_ms=round(1e3 * float(t.mean()), 4),
+            detail=dict(grid=[g_ctas.value, g_thr.value], hm_gteps_rank0=round(hm, 4), mean_ms=round(1e3 * float(t.mean()), 4),
                         min_ms=round(1e3 * float(t.min()), 4), max_ms=round(1e3 * float(t.max()), 4),
                         mean_dequeues=int(np.mean([c["D"] for c in census])),
                         mean_levels=float(np.mean([c["L"] for c in census])),

@@ -34,13 +34,14 @@
 
 #include "bfs.cuh"
 #include "bfs_device.cuh"
+#include "sigma.cuh"
 
 namespace blestgpu {
 
 extern std::atomic<uint64_t> g_launches;
 
 void* eager_kernel(int pull, int threads);       // bfs_eager.cu
-void* lazy_kernel(int pull, int threads);        // bfs_lazy.cu
+void* lazy_kernel(int pull, int threads, bool sigma);  // bfs_lazy.cu
 void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
 size_t lazy_tma_smem(int consumers);
 
@@ -109,13 +110,15 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     const bool lazy_tma = opt.mode == Mode::Lazy && (opt.lazy_tma || (var_env && std::string(var_env) == "tma"));
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
     const int consumers = nc_env ? atoi(nc_env) : 8;
+    const char* sig_env = getenv("BLEST_SIGMA");
+    const bool sigma = opt.mode == Mode::Lazy && !lazy_tma && opt.sigma && !(sig_env && atoi(sig_env) == 0);
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
         kern = eager_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
     else
         kern = lazy_tma ? lazy_tma_kernel(opt.pull == Pull::Mma ? 1 : 0, consumers)
-                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads);
+                        : lazy_kernel(opt.pull == Pull::Mma ? 1 : 0, threads, sigma);
     size_t dyn = 0;
     if (lazy_tma) {
         dyn = lazy_tma_smem(consumers);
@@ -157,6 +160,16 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
+    if (sigma) {
+        if (!sigma_built_) {
+            sigma_view_build(b_, sigma_);
+            sigma_built_ = true;
+        }
+        p.rows4 = reinterpret_cast<const uint4*>(sigma_.rows.p);
+        p.inv = sigma_.inv.p;
+        p.sig = sigma_.sig.p;
+    }
+    if (const char* rc = getenv("BLEST_LAZY_RECHECK")) p.lazy_recheck = (uint32_t)atoi(rc);
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
     if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);

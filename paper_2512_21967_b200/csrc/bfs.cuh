@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "bvss.cuh"
+#include "sigma.cuh"
 
 namespace blestgpu {
 
@@ -20,6 +21,7 @@ struct EngineOptions {
     uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
+    bool sigma = true;        // lazy: visited bitmaps in frequency-ranked row space (sigma.cuh)
     bool lazy_tma = false;    // lazy: TMA producer/consumer pipeline (measured slower on C2)
 };
 
@@ -79,6 +81,8 @@ private:
     DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA VSS counts
     DevBuf<unsigned long long> aggS_;    // lazy stage-2 per-CTA slice-set counts
     DevBuf<unsigned long long> sl_;      // lazy queue: active slice sets
+    SigmaView sigma_;                    // lazy: built on the first σ launch
+    bool sigma_built_ = false;
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
     DevBuf<unsigned long long> tstamp_;  // trace_cap_ * 3

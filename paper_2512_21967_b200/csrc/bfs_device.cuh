@@ -41,7 +41,12 @@ struct Params {
     uint32_t cap;
     uint32_t num_warps;
     uint64_t dense_min;  // queue length from which a level counts as dense (eager re-checks)
+    // lazy σ view (sigma.cuh): V_curr / V_next (B0, B1) in σ space, σ⁻¹ and σ; the
+    // levels L and the frontier diff Fd (B2) stay in original space
+    const uint32_t* __restrict__ inv;
+    const uint32_t* __restrict__ sig;
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
+    uint32_t lazy_recheck;  // lazy: test V_curr and re-check V_next at L2 (BLEST_LAZY_RECHECK)
 };
 
 template <int THREADS, int MODE = 0>
@@ -376,6 +381,79 @@ __device__ __forceinline__ void s2_load(const Params& p, const uint32_t* src, ui
     }
 }
 
+// Second half of stage 2 (shared by both stage-2 variants): publish the CTA's (VSS, set)
+// counts tagged with the level, sum its predecessors', and write its SL entries from the
+// frontier diff words of its chunks (`keep` holds them when the CTA owns one chunk).
+template <int THREADS>
+__device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm, uint32_t level, uint32_t (&ctr)[4],
+                                           uint64_t k0, uint64_t k1, bool single, const uint32_t (&keep)[4],
+                                           unsigned long long my_vss, unsigned long long my_sets) {
+    constexpr unsigned long long kTagMask = (1ull << 40) - 1;
+    constexpr uint64_t CH = 4ull * THREADS;
+    const uint32_t* Fd = p.B2;
+    unsigned long long cta_vss = 0, cta_sets = 0;
+    block_excl_scan(sm, my_vss, &cta_vss);
+    block_excl_scan(sm, my_sets, &cta_sets);
+    if (threadIdx.x == 0) {
+        const unsigned long long tag = (unsigned long long)level << 40;
+        p.aggS[blockIdx.x] = tag | cta_sets;
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag | cta_vss) : "memory");
+    }
+    unsigned long long bv = 0, bs = 0;
+    for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
+        unsigned long long x;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
+        } while ((x >> 40) != level);
+        bv += x & kTagMask;
+        bs += ld_relaxed_gpu_u64(p.aggS + c) & kTagMask;
+    }
+    unsigned long long run_vss = 0, run_sets = 0;
+    block_excl_scan(sm, bv, &run_vss);
+    block_excl_scan(sm, bs, &run_sets);
+    if (threadIdx.x == 0) {
+        ctr[3] += (uint32_t)cta_vss;
+        if (blockIdx.x == gridDim.x - 1) {  // grid totals: the next level's T, S
+            p.ctl[0] = run_vss + cta_vss;
+            p.ctl[1] = run_sets + cta_sets;
+        }
+    }
+    // pass B: SL entries of the CTA's active sets, ascending
+    for (uint64_t ch = k0; ch < k1; ++ch) {
+        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
+        uint32_t d[4];
+        if (single) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) d[k] = keep[k];
+        } else {
+            s2_load<THREADS>(p, Fd, w0, d, true);
+        }
+        unsigned long long nv = 0, ns = 0;
+        s2_counts<THREADS>(p, w0, d, nv, ns);
+        unsigned long long it_v = 0, it_s = 0;
+        unsigned long long pv = run_vss + block_excl_scan(sm, nv, &it_v);
+        unsigned long long ps = run_sets + block_excl_scan(sm, ns, &it_s);
+        if (ns) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if ((d[k] >> (8 * b)) & 0xFFu) {
+                        const uint64_t ss = 4 * (w0 + k) + b;
+                        const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
+                        if (c) {
+                            p.SL[ps++] = (pv << 32) | ss;
+                            pv += c;
+                        }
+                    }
+                }
+            }
+        }
+        run_vss += it_v;
+        run_sets += it_s;
+    }
+}
+
 template <int THREADS>
 __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
                                             uint32_t (&ctr)[4]) {
@@ -430,67 +508,87 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
             }
         }
     }
-    unsigned long long cta_vss = 0, cta_sets = 0;
-    block_excl_scan(sm, my_vss, &cta_vss);
-    block_excl_scan(sm, my_sets, &cta_sets);
-    if (threadIdx.x == 0) {
-        const unsigned long long tag = (unsigned long long)level << 40;
-        p.aggS[blockIdx.x] = tag | cta_sets;
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.agg + blockIdx.x), "l"(tag | cta_vss) : "memory");
-    }
-    unsigned long long bv = 0, bs = 0;
-    for (uint32_t c = threadIdx.x; c < blockIdx.x; c += THREADS) {
-        unsigned long long x;
-        do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p.agg + c) : "memory");
-        } while ((x >> 40) != level);
-        bv += x & kTagMask;
-        bs += ld_relaxed_gpu_u64(p.aggS + c) & kTagMask;
-    }
-    unsigned long long run_vss = 0, run_sets = 0;
-    block_excl_scan(sm, bv, &run_vss);
-    block_excl_scan(sm, bs, &run_sets);
-    if (threadIdx.x == 0) {
-        ctr[3] += (uint32_t)cta_vss;
-        if (blockIdx.x == gridDim.x - 1) {  // grid totals: the next level's T, S
-            p.ctl[0] = run_vss + cta_vss;
-            p.ctl[1] = run_sets + cta_sets;
+    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets);
+}
+
+// σ-space stage 2 (sigma.cuh): pass S over the σ-space words — diff = V_next & ~V_curr,
+// V_curr = V_next, and each discovery mapped back (σ⁻¹, one coalesced 128 B read per
+// changed word) to store its level in L and RED its bit into the original-space frontier
+// diff Fd (zeroed during stage 1); a grid barrier; then the original-space diff words are
+// counted and enqueued like lazy_stage2.
+template <int THREADS>
+__device__ __forceinline__ void lazy_stage2_sigma(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
+                                                  uint32_t (&ctr)[4], unsigned& gen) {
+    constexpr uint64_t CH = 4ull * THREADS;
+    const unsigned lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    uint32_t* Vc = p.B0;
+    uint32_t* Vn = p.B1;
+    uint32_t* Fd = p.B2;
+    const uint64_t chunks = (p.words + CH - 1) / CH;
+    const uint64_t k0 = (uint64_t)blockIdx.x * chunks / gridDim.x, k1 = (uint64_t)(blockIdx.x + 1) * chunks / gridDim.x;
+    const bool single = k1 - k0 <= 1;
+    for (uint64_t ch = k0; ch < k1; ++ch) {
+        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
+        uint32_t nx[4], cu[4], d[4];
+        s2_load<THREADS>(p, Vn, w0, nx, true);
+        s2_load<THREADS>(p, Vc, w0, cu, false);
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            d[k] = nx[k] & ~cu[k];
+            any |= d[k] != 0;
+            ctr[0] += __popc(d[k]);
+        }
+        if (any) {
+            if (w0 + 4 <= p.words) {
+                *reinterpret_cast<uint4*>(Vc + w0) = make_uint4(nx[0], nx[1], nx[2], nx[3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (w0 + k < p.words && d[k]) Vc[w0 + k] = nx[k];
+            }
+        }
+        // Changed words, 8 at a time: lanes = bits; the 8 σ⁻¹ reads (coalesced 128 B each)
+        // are in flight together before their REDs (the hot, dense head of σ space gets
+        // most discoveries of the early levels, all in the first CTA's chunk).
+        const uint64_t wwarp = ch * CH + 128ull * warp;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            unsigned bk = __ballot_sync(0xffffffffu, d[k] != 0);
+            while (bk) {
+                uint32_t dk[8], rr[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int src = bk ? __ffs(bk) - 1 : 0;
+                    dk[t] = bk ? __shfl_sync(0xffffffffu, d[k], src) : 0u;
+                    bk &= bk - 1;
+                    const uint64_t q = 32 * (wwarp + 4 * (uint64_t)src + k) + lane;
+                    rr[t] = ((dk[t] >> lane) & 1u) ? __ldg(p.inv + q) : 0u;
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if ((dk[t] >> lane) & 1u) {
+                        p.L[rr[t]] = level;  // scattered, but L (67 MB at C2) stays in L2
+                        red_or(Fd + (rr[t] >> 5), 1u << (rr[t] & 31));
+                    }
+            }
         }
     }
-    // pass B: SL entries of the CTA's active sets, ascending
+    grid_barrier(p.bar, gen);  // the scattered frontier is complete
+    if ((p.xflags & 32) && blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
+        p.tstamp[3ull * (level - 1) + 1] = globaltimer();  // timing study: pass S end
+    uint32_t keep[4] = {0, 0, 0, 0};
+    unsigned long long my_vss = 0, my_sets = 0;
     for (uint64_t ch = k0; ch < k1; ++ch) {
         const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
         uint32_t d[4];
-        if (single) {
+        s2_load<THREADS>(p, Fd, w0, d, true);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) d[k] = keep[k];
-        } else {
-            s2_load<THREADS>(p, Fd, w0, d, false);
-        }
-        unsigned long long nv = 0, ns = 0;
-        s2_counts<THREADS>(p, w0, d, nv, ns);
-        unsigned long long it_v = 0, it_s = 0;
-        unsigned long long pv = run_vss + block_excl_scan(sm, nv, &it_v);
-        unsigned long long ps = run_sets + block_excl_scan(sm, ns, &it_s);
-        if (ns) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    if ((d[k] >> (8 * b)) & 0xFFu) {
-                        const uint64_t ss = 4 * (w0 + k) + b;
-                        const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
-                        if (c) {
-                            p.SL[ps++] = (pv << 32) | ss;
-                            pv += c;
-                        }
-                    }
-                }
-            }
-        }
-        run_vss += it_v;
-        run_sets += it_s;
+        for (int k = 0; k < 4; ++k) keep[k] = d[k];
+        s2_counts<THREADS>(p, w0, d, my_vss, my_sets);
     }
+    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets);
 }
 
 }  // namespace bfsdev

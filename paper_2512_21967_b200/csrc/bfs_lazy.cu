@@ -29,17 +29,24 @@ using namespace bfsdev;
 #ifndef BLEST_MINB
 #define BLEST_MINB 1
 #endif
-// Visited tests of one batch (kBatch VSSs × 4 columns per lane) in three batch-wide phases,
+// Visited tests of one batch (kBatch VSSs × 4 columns per lane) in batch-wide phases,
 // each phase's memory operations in flight together (one latency per phase, not one per
-// VSS): (A) for every column with a nonzero pull, visited before this level? — V_curr
-// (frozen, L1); (B) for the rest, marked this level already? — V_next at L2 (skipped with
-// xflags bit 2); (C) a fire-and-forget RED for what is still clear. Branch-free PTX blocks
-// (bfs_device.cuh). rows(j) / mask(j) give the lane's row ids and mask word of VSS j; the
-// row ids are re-read per phase, so a shared-memory source keeps them out of registers.
-// Returns the number of REDs issued.
+// VSS): (A) for every column with a nonzero pull, the row's word of the test bitmap W —
+// a plain, L1-cached load; (B) optionally (Params::recheck) the words still clear re-read
+// from V_next at L2; (C) a fire-and-forget RED into V_next for every bit still clear
+// (legal per SURVEY §8(a) pitfall 7). Default W = V_next without (B): V_next ⊇ V_curr, so
+// a set bit means "visited before, or already marked this level", and an L1 copy lagging
+// this level's REDs from other SMs only costs an extra idempotent RED (the grid barrier
+// invalidates L1 between levels). W = V_curr with (B) is the older scheme (V_curr is
+// frozen within the level; the L2 re-check spares REDs). Measured on C2: 2.35 → 2.01 ms
+// per BFS for the default. Branch-free PTX blocks (bfs_device.cuh); rows(j) / mask(j)
+// give the lane's row ids and mask word of VSS j. Returns the number of REDs issued.
+// (Codegen note: the optional phase B branch also keeps ptxas from interleaving phase
+// A's result moves with its later loads — without it the same default path measured
+// 5.3 ms per BFS.)
 template <int PULL, typename Rows, typename Mask>
-__device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t* Vc, uint32_t* Vn, unsigned long long e,
-                                                Rows rows, Mask mask) {
+__device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t* W, uint32_t* Vn, bool recheck,
+                                                unsigned long long e, Rows rows, Mask mask) {
     uint32_t vw[4 * kBatch];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
@@ -66,17 +73,15 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
             }
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            vw[4 * j + c] = cand_word(Vc, u[c], m[c], sel[c]);
+        for (int c = 0; c < 4; ++c) vw[4 * j + c] = cand_word(W, u[c], m[c], sel[c]);
     }
-    if (!(p.xflags & 2)) {
+    if (recheck) {
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const uint4 r = rows(j);
             const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                vw[4 * j + c] = recheck_word(Vn, u[c], vw[4 * j + c]);
+            for (int c = 0; c < 4; ++c) vw[4 * j + c] = recheck_word(Vn, u[c], vw[4 * j + c]);
         }
     }
     uint32_t reds = 0;
@@ -85,14 +90,12 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
         const uint4 r = rows(j);
         const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            reds += red_if_clear(Vn, u[c], vw[4 * j + c]);
-        }
+        for (int c = 0; c < 4; ++c) reds += red_if_clear(Vn, u[c], vw[4 * j + c]);
     }
     return reds;
 }
 
-template <int PULL, int THREADS>
+template <int PULL, int THREADS, bool SIGMA>
 __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)) k_bfs_lazy(Params p) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
@@ -109,19 +112,21 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
     uint32_t* Fd = p.B2;
-    const uint4* __restrict__ rows4 = p.rows4;
+    const uint4* __restrict__ rows4 = p.rows4;  // SIGMA: the σ view's row ids
 
     // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
     const uint32_t src = p.src;
     const uint32_t sset = src / kSigma;
     const uint32_t seed_b = p.rp[sset], seed_e = p.rp[sset + 1];
+    const uint32_t vsrc = SIGMA ? p.sig[src] : src;  // the source in the visited bitmaps' space
     for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
     const uint32_t src_word = src >> 5, src_bit = 1u << (src & 31);
+    const uint32_t vs_word = vsrc >> 5, vs_bit = 1u << (vsrc & 31);
     for (uint64_t w = gtid; w < p.words; w += gthreads) {
-        const uint32_t seed = (w == src_word) ? src_bit : 0u;
+        const uint32_t seed = (w == vs_word) ? vs_bit : 0u;
         Vc[w] = seed;
         Vn[w] = seed;
-        Fd[w] = seed;  // α of the source's set for level 1
+        Fd[w] = (w == src_word) ? src_bit : 0u;  // α of the source's set for level 1
     }
     if (threadIdx.x == 0) {
         p.agg[blockIdx.x] = 0;
@@ -187,12 +192,16 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         }
         grid_barrier(p.bar, gen);
 
+        if (SIGMA)  // the expansion has read α: clear Fd for stage 2's scattered discoveries
+            for (uint64_t w = gtid; w < p.words; w += gthreads) Fd[w] = 0;
         // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
             // Position walk: round-robin over all warps like the reference (p ≡ warp mod
             // #warps, :190). (A CTA-contiguous walk, for L1 sharing among an SM's warps,
             // measured no better.)
             const uint64_t qstride = NW, q0 = gw, qend = len;
+            const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
+            const uint32_t* W = recheck ? Vc : Vn;
             const uint64_t step = qstride * kBatch;
             auto qload = [&](uint64_t base) -> unsigned long long {
                 const uint64_t pos = base + (uint64_t)lane * qstride;
@@ -214,12 +223,16 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                     mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
                     rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
                 }
-                ctr[2] += check_batch<PULL>(p, Vc, Vn, e, [&](int j) { return rw[j]; }, [&](int j) { return mk[j]; });
+                ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
+                                            [&](int j) { return mk[j]; });
             }
         }
         level_barrier(p, sm, gen, level, ctr, 1);
 
-        lazy_stage2<THREADS>(p, sm, level, ctr);
+        if (SIGMA)
+            lazy_stage2_sigma<THREADS>(p, sm, level, ctr, gen);
+        else
+            lazy_stage2<THREADS>(p, sm, level, ctr);
         next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
@@ -227,20 +240,19 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
 
 }  // namespace
 
-void* lazy_kernel(int pull, int threads) {
-    if (pull == 1) {
-        switch (threads) {
-            case 256: return (void*)k_bfs_lazy<1, 256>;
-            case 512: return (void*)k_bfs_lazy<1, 512>;
-            case 1024: return (void*)k_bfs_lazy<1, 1024>;
-        }
-    } else {
-        switch (threads) {
-            case 256: return (void*)k_bfs_lazy<0, 256>;
-            case 512: return (void*)k_bfs_lazy<0, 512>;
-            case 1024: return (void*)k_bfs_lazy<0, 1024>;
-        }
+void* lazy_kernel(int pull, int threads, bool sigma) {
+#define BLEST_LAZY_CASES(PULL, SIGMA)                         \
+    switch (threads) {                                        \
+        case 256: return (void*)k_bfs_lazy<PULL, 256, SIGMA>;   \
+        case 512: return (void*)k_bfs_lazy<PULL, 512, SIGMA>;   \
+        case 1024: return (void*)k_bfs_lazy<PULL, 1024, SIGMA>; \
     }
+    if (pull == 1) {
+        if (sigma) { BLEST_LAZY_CASES(1, true) } else { BLEST_LAZY_CASES(1, false) }
+    } else {
+        if (sigma) { BLEST_LAZY_CASES(0, true) } else { BLEST_LAZY_CASES(0, false) }
+    }
+#undef BLEST_LAZY_CASES
     throw InvalidArgument("threads per CTA must be 256, 512 or 1024");
 }
 

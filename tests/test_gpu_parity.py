@@ -247,14 +247,16 @@ def test_auto_pipeline_maps_levels_back(oracle):
 
 @pytest.mark.parametrize("env", [
     {},
-    {"BLEST_XFLAGS": "2"},                 # lazy: no V_next re-check before the RED
+    {"BLEST_SIGMA": "0"},                  # lazy: visited bitmaps by plain row id (no σ view)
+    {"BLEST_LAZY_RECHECK": "1"},           # lazy: test V_curr, re-check V_next at L2
     {"BLEST_DENSE_MIN": "1"},              # eager: F_next re-check on every level
     {"BLEST_DENSE_MIN": "1000000000"},     # eager: never (straight to the atomic)
 ])
 def test_engine_phase_variants(oracle, monkeypatch, env):
-    """The batch-wide visited-test phases and their switches change only how the tests are
-    answered: levels and every deterministic counter equal the reference engine's, for both
-    engines and pulls, on undirected and directed graphs, including a hub source."""
+    """The batch-wide visited-test phases, the lazy σ view and their switches change only how
+    the tests are answered: levels and every deterministic counter equal the reference
+    engine's, for both engines and pulls, on undirected and directed graphs, including the
+    most connected (first in σ) vertex as source."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for directed in (False, True):
