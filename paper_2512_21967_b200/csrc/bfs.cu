@@ -162,14 +162,20 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.num_warps = opt.num_warps;
     if (sigma) {
         if (!sigma_built_) {
-            sigma_view_build(b_, sigma_);
+            const char* hot = getenv("BLEST_HOT");
+            sigma_view_build(b_, sigma_, hot ? (uint32_t)atoll(hot) : 0u);
+            const uint64_t stride = sigma_.hot_words + wstride_;  // both multiples of 4 words
+            vext_.alloc(2 * stride);
             sigma_built_ = true;
         }
+        const uint64_t stride = sigma_.hot_words + wstride_;
+        p.B0 = vext_.p;  // V_curr / V_next = [hot prefix | row words]
+        p.B1 = vext_.p + stride;
         p.rows4 = reinterpret_cast<const uint4*>(sigma_.rows.p);
         p.inv = sigma_.inv.p;
         p.sig = sigma_.sig.p;
+        p.hot_words = sigma_.hot_words;
     }
-    if (const char* rc = getenv("BLEST_LAZY_RECHECK")) p.lazy_recheck = (uint32_t)atoi(rc);
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
     if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);

@@ -21,7 +21,7 @@ struct EngineOptions {
     uint32_t num_warps = 0;   // logical warps for the round-robin VSS split; 0 = whole grid
     uint32_t grid_ctas = 0;   // 0 = every co-resident CTA (persistent grid)
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
-    bool sigma = true;        // lazy: visited bitmaps in frequency-ranked row space (sigma.cuh)
+    bool sigma = true;        // lazy: hot-row view of the visited bitmaps (sigma.cuh)
     bool lazy_tma = false;    // lazy: TMA producer/consumer pipeline (measured slower on C2)
 };
 
@@ -81,7 +81,8 @@ private:
     DevBuf<unsigned long long> agg_;     // lazy stage-2 per-CTA VSS counts
     DevBuf<unsigned long long> aggS_;    // lazy stage-2 per-CTA slice-set counts
     DevBuf<unsigned long long> sl_;      // lazy queue: active slice sets
-    SigmaView sigma_;                    // lazy: built on the first σ launch
+    SigmaView sigma_;                    // lazy: hot-row view, built on the first lazy launch
+    DevBuf<uint32_t> vext_;              // lazy hot-row view: V_curr, V_next with the hot prefix
     bool sigma_built_ = false;
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8

@@ -41,10 +41,11 @@ struct Params {
     uint32_t cap;
     uint32_t num_warps;
     uint64_t dense_min;  // queue length from which a level counts as dense (eager re-checks)
-    // lazy σ view (sigma.cuh): V_curr / V_next (B0, B1) in σ space, σ⁻¹ and σ; the
-    // levels L and the frontier diff Fd (B2) stay in original space
+    // lazy hot-row view (sigma.cuh): V_curr / V_next (B0, B1) = [hot prefix, hot_words
+    // words | row words]; inv: hot rank -> row; sig: row -> engine id (source seeding)
     const uint32_t* __restrict__ inv;
     const uint32_t* __restrict__ sig;
+    uint64_t hot_words;
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
     uint32_t lazy_recheck;  // lazy: test V_curr and re-check V_next at L2 (BLEST_LAZY_RECHECK)
 };
@@ -454,47 +455,53 @@ __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm
     }
 }
 
-template <int THREADS>
+// HOT (hot-row view, sigma.cuh): the visited words of row r live at word r/32 + hot_words
+// (after the hot prefix), and Fd already holds the hot rows' discoveries (REDs of
+// hot_stage2), which are merged into the frontier words; their levels are already stored.
+template <int THREADS, bool HOT = false>
 __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
                                             uint32_t (&ctr)[4]) {
     constexpr unsigned long long kTagMask = (1ull << 40) - 1;
     constexpr uint64_t CH = 4ull * THREADS;
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
-    uint32_t* Vc = p.B0;
-    uint32_t* Vn = p.B1;
+    uint32_t* Vc = p.B0 + (HOT ? p.hot_words : 0);  // 16-byte aligned: hot_words % 4 == 0
+    uint32_t* Vn = p.B1 + (HOT ? p.hot_words : 0);
     uint32_t* Fd = p.B2;
     const uint64_t chunks = (p.words + CH - 1) / CH;
     const uint64_t k0 = (uint64_t)blockIdx.x * chunks / gridDim.x, k1 = (uint64_t)(blockIdx.x + 1) * chunks / gridDim.x;
     const bool single = k1 - k0 <= 1;
-    uint32_t keep[4] = {0, 0, 0, 0};  // diff words of the CTA's only chunk
+    uint32_t keep[4] = {0, 0, 0, 0};  // frontier words of the CTA's only chunk
     unsigned long long my_vss = 0, my_sets = 0;
     // pass A
     for (uint64_t ch = k0; ch < k1; ++ch) {
         const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
-        uint32_t nx[4], cu[4], d[4];
+        uint32_t nx[4], cu[4], d[4], f[4];
         s2_load<THREADS>(p, Vn, w0, nx, true);  // REDs landed in L2
         s2_load<THREADS>(p, Vc, w0, cu, false);
+        if (HOT) s2_load<THREADS>(p, Fd, w0, f, true);  // hot rows' discoveries (REDs)
         bool any = false;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             d[k] = nx[k] & ~cu[k];
             any |= d[k] != 0;
             ctr[0] += __popc(d[k]);
-            keep[k] = d[k];
+            if (HOT) f[k] |= d[k];
+            else f[k] = d[k];
+            keep[k] = f[k];
         }
         if (w0 + 4 <= p.words) {
-            *reinterpret_cast<uint4*>(Fd + w0) = make_uint4(d[0], d[1], d[2], d[3]);
+            *reinterpret_cast<uint4*>(Fd + w0) = make_uint4(f[0], f[1], f[2], f[3]);
             if (any) *reinterpret_cast<uint4*>(Vc + w0) = make_uint4(nx[0], nx[1], nx[2], nx[3]);
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (w0 + k < p.words) {
-                    Fd[w0 + k] = d[k];
+                    Fd[w0 + k] = f[k];
                     if (d[k]) Vc[w0 + k] = nx[k];
                 }
         }
-        s2_counts<THREADS>(p, w0, d, my_vss, my_sets);
+        s2_counts<THREADS>(p, w0, f, my_vss, my_sets);
         // levels: one coalesced 128 B store per changed word (lane = bit)
         unsigned ball = __ballot_sync(0xffffffffu, any);
         const uint64_t wwarp = ch * CH + 128ull * warp;
@@ -511,84 +518,47 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
     s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets);
 }
 
-// σ-space stage 2 (sigma.cuh): pass S over the σ-space words — diff = V_next & ~V_curr,
-// V_curr = V_next, and each discovery mapped back (σ⁻¹, one coalesced 128 B read per
-// changed word) to store its level in L and RED its bit into the original-space frontier
-// diff Fd (zeroed during stage 1); a grid barrier; then the original-space diff words are
-// counted and enqueued like lazy_stage2.
+// Hot-row stage 2 (sigma.cuh): the hot prefix of the visited bitmaps (hot_words words,
+// one per thread) — diff, V_curr update, and each hot discovery mapped back (σ⁻¹) to store
+// its level and RED its bit into the original-space frontier Fd (zeroed during stage 1);
+// a grid barrier; then lazy_stage2<HOT> sweeps the row words and merges Fd.
 template <int THREADS>
-__device__ __forceinline__ void lazy_stage2_sigma(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
-                                                  uint32_t (&ctr)[4], unsigned& gen) {
-    constexpr uint64_t CH = 4ull * THREADS;
-    const unsigned lane = lane_id();
-    const uint32_t warp = threadIdx.x >> 5;
+__device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
+                                                uint32_t (&ctr)[4], unsigned& gen) {
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
     uint32_t* Fd = p.B2;
-    const uint64_t chunks = (p.words + CH - 1) / CH;
-    const uint64_t k0 = (uint64_t)blockIdx.x * chunks / gridDim.x, k1 = (uint64_t)(blockIdx.x + 1) * chunks / gridDim.x;
-    const bool single = k1 - k0 <= 1;
-    for (uint64_t ch = k0; ch < k1; ++ch) {
-        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
-        uint32_t nx[4], cu[4], d[4];
-        s2_load<THREADS>(p, Vn, w0, nx, true);
-        s2_load<THREADS>(p, Vc, w0, cu, false);
-        bool any = false;
+    const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    const uint64_t gthreads = (uint64_t)gridDim.x * THREADS;
+    for (uint64_t w = gtid; w < p.hot_words; w += gthreads) {
+        const uint32_t nx = __ldcg(Vn + w), d = nx & ~Vc[w];
+        if (!d) continue;
+        Vc[w] = nx;
+        ctr[0] += __popc(d);
+        for (uint32_t rest = d; rest;) {  // σ⁻¹ reads 8 at a time, then their stores / REDs
+            uint32_t rr[8], bits = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            d[k] = nx[k] & ~cu[k];
-            any |= d[k] != 0;
-            ctr[0] += __popc(d[k]);
-        }
-        if (any) {
-            if (w0 + 4 <= p.words) {
-                *reinterpret_cast<uint4*>(Vc + w0) = make_uint4(nx[0], nx[1], nx[2], nx[3]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (w0 + k < p.words && d[k]) Vc[w0 + k] = nx[k];
-            }
-        }
-        // Changed words, 8 at a time: lanes = bits; the 8 σ⁻¹ reads (coalesced 128 B each)
-        // are in flight together before their REDs (the hot, dense head of σ space gets
-        // most discoveries of the early levels, all in the first CTA's chunk).
-        const uint64_t wwarp = ch * CH + 128ull * warp;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            unsigned bk = __ballot_sync(0xffffffffu, d[k] != 0);
-            while (bk) {
-                uint32_t dk[8], rr[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int src = bk ? __ffs(bk) - 1 : 0;
-                    dk[t] = bk ? __shfl_sync(0xffffffffu, d[k], src) : 0u;
-                    bk &= bk - 1;
-                    const uint64_t q = 32 * (wwarp + 4 * (uint64_t)src + k) + lane;
-                    rr[t] = ((dk[t] >> lane) & 1u) ? __ldg(p.inv + q) : 0u;
+            for (int t = 0; t < 8; ++t) {
+                rr[t] = 0;
+                if (rest) {
+                    const int b = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    rr[t] = __ldg(p.inv + 32 * w + b);
+                    bits |= 1u << t;
                 }
-#pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    if ((dk[t] >> lane) & 1u) {
-                        p.L[rr[t]] = level;  // scattered, but L (67 MB at C2) stays in L2
-                        red_or(Fd + (rr[t] >> 5), 1u << (rr[t] & 31));
-                    }
             }
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if ((bits >> t) & 1u) {
+                    p.L[rr[t]] = level;
+                    red_or(Fd + (rr[t] >> 5), 1u << (rr[t] & 31));
+                }
         }
     }
-    grid_barrier(p.bar, gen);  // the scattered frontier is complete
+    grid_barrier(p.bar, gen);  // the hot discoveries are in Fd
     if ((p.xflags & 32) && blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
-        p.tstamp[3ull * (level - 1) + 1] = globaltimer();  // timing study: pass S end
-    uint32_t keep[4] = {0, 0, 0, 0};
-    unsigned long long my_vss = 0, my_sets = 0;
-    for (uint64_t ch = k0; ch < k1; ++ch) {
-        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
-        uint32_t d[4];
-        s2_load<THREADS>(p, Fd, w0, d, true);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) keep[k] = d[k];
-        s2_counts<THREADS>(p, w0, d, my_vss, my_sets);
-    }
-    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets);
+        p.tstamp[3ull * (level - 1) + 1] = globaltimer();  // timing study: hot pass end
+    lazy_stage2<THREADS, true>(p, sm, level, ctr);
 }
 
 }  // namespace bfsdev

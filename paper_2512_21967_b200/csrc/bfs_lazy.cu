@@ -118,15 +118,17 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
     const uint32_t src = p.src;
     const uint32_t sset = src / kSigma;
     const uint32_t seed_b = p.rp[sset], seed_e = p.rp[sset + 1];
-    const uint32_t vsrc = SIGMA ? p.sig[src] : src;  // the source in the visited bitmaps' space
+    const uint32_t vsrc = SIGMA ? p.sig[src] : src;  // the source's engine id (hot rank or row)
     for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
     const uint32_t src_word = src >> 5, src_bit = 1u << (src & 31);
-    const uint32_t vs_word = vsrc >> 5, vs_bit = 1u << (vsrc & 31);
-    for (uint64_t w = gtid; w < p.words; w += gthreads) {
+    const uint64_t vs_word = vsrc >> 5;
+    const uint32_t vs_bit = 1u << (vsrc & 31);
+    const uint64_t vwords = p.words + (SIGMA ? p.hot_words : 0);  // visited bitmap words
+    for (uint64_t w = gtid; w < vwords; w += gthreads) {
         const uint32_t seed = (w == vs_word) ? vs_bit : 0u;
         Vc[w] = seed;
         Vn[w] = seed;
-        Fd[w] = (w == src_word) ? src_bit : 0u;  // α of the source's set for level 1
+        if (w < p.words) Fd[w] = (w == src_word) ? src_bit : 0u;  // α of the source's set, level 1
     }
     if (threadIdx.x == 0) {
         p.agg[blockIdx.x] = 0;
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
         level_barrier(p, sm, gen, level, ctr, 1);
 
         if (SIGMA)
-            lazy_stage2_sigma<THREADS>(p, sm, level, ctr, gen);
+            lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen);
         else
             lazy_stage2<THREADS>(p, sm, level, ctr);
         next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);

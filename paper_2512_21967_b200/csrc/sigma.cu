@@ -1,6 +1,9 @@
-// σ view builder (see sigma.cuh): slot histogram -> one 64-bit radix sort of
-// (UINT32_MAX - count, row) -> σ / σ⁻¹ -> engine copy of row_ids.
+// Hot-row view builder (see sigma.cuh): slot histogram -> one 64-bit radix sort of
+// (UINT32_MAX - count, row) -> engine ids (hot ranks, shifted rows) and σ⁻¹ of the hot
+// ranks -> engine copy of row_ids.
 #include <cub/cub.cuh>
+
+#include <algorithm>
 
 #include "sigma.cuh"
 
@@ -25,24 +28,19 @@ __global__ void k_rank_keys(const uint32_t* __restrict__ cnt, uint32_t n, uint64
         keys[r] = ((uint64_t)(0xFFFFFFFFu - cnt[r]) << 32) | r;
 }
 
-// Rank q -> σ id: ranks stay contiguous within 128 B lines (1024 ids, the L1 unit), but the
-// lines are dealt round-robin over kSpread stripes of σ space, so the hottest lines — the
-// bulk of the early levels' discoveries — spread over all stage-2 chunks instead of one.
-// Bijective: lines [0, B) with B = kSpread·⌊lines / kSpread⌋ are transposed, the rest kept.
-constexpr uint32_t kSpread = 256;
-__global__ void k_sigma_tables(const uint64_t* __restrict__ keys, uint32_t n, uint32_t* __restrict__ sig,
-                               uint32_t* __restrict__ inv) {
-    const uint64_t lines = ((uint64_t)n + 1023) / 1024;
-    const uint64_t per = lines / kSpread, B = per * kSpread;
-    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+__global__ void k_engine_ids(uint32_t n, uint32_t base, uint32_t* __restrict__ sig) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+         r += (uint64_t)gridDim.x * blockDim.x)
+        sig[r] = base + (uint32_t)r;
+}
+
+__global__ void k_hot_tables(const uint64_t* __restrict__ keys, uint32_t K, uint32_t* __restrict__ sig,
+                             uint32_t* __restrict__ inv) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < K;
          q += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t r = (uint32_t)keys[q];
-        const uint64_t line = q >> 10;
-        const uint64_t l2 = line < B ? (line % kSpread) * per + line / kSpread : line;
-        const uint64_t id = (l2 << 10) | (q & 1023);
-        // the last (partial) line keeps its ids < n; a full transposed line maps in range
-        inv[id] = r;
-        sig[r] = (uint32_t)id;
+        inv[q] = r;
+        sig[r] = (uint32_t)q;
     }
 }
 
@@ -61,12 +59,16 @@ __global__ void k_sigma_rows(const uint4* __restrict__ rows, uint64_t n4, uint32
 
 }  // namespace
 
-void sigma_view_build(const DeviceBvss& b, SigmaView& out) {
+void sigma_view_build(const DeviceBvss& b, SigmaView& out, uint32_t hot_cap) {
     cudaStream_t st = stream();
     const uint32_t n = b.n;
     const uint64_t slots = (uint64_t)b.num_vss * kTau;
+    if (!hot_cap) hot_cap = 1u << 20;
+    out.K = std::min(n, hot_cap);
+    out.hot_words = ((uint64_t)out.K + 127) / 128 * 4;  // whole uint4 granules
+    if (32 * out.hot_words + n >= (1ull << 32)) throw InvalidArgument("hot-row view needs n < 2^32 - K");
     out.sig.alloc(n ? n : 1);
-    out.inv.alloc(n ? n : 1);
+    out.inv.alloc(out.K ? out.K : 1);
     if (n) {
         DevBuf<uint32_t> cnt(n);
         CK(cudaMemsetAsync(cnt.p, 0, (size_t)n * 4, st));
@@ -77,7 +79,8 @@ void sigma_view_build(const DeviceBvss& b, SigmaView& out) {
         CK(cub::DeviceRadixSort::SortKeys(nullptr, temp, keys.p, keys2.p, (int64_t)n, 0, 64, st));
         DevBuf<unsigned char> tmp(temp ? temp : 1);
         CK(cub::DeviceRadixSort::SortKeys(tmp.p, temp, keys.p, keys2.p, (int64_t)n, 0, 64, st));
-        k_sigma_tables<<<grid_for(n, 256), 256, 0, st>>>(keys2.p, n, out.sig.p, out.inv.p);
+        k_engine_ids<<<grid_for(n, 256), 256, 0, st>>>(n, (uint32_t)(32 * out.hot_words), out.sig.p);
+        if (out.K) k_hot_tables<<<grid_for(out.K, 256), 256, 0, st>>>(keys2.p, out.K, out.sig.p, out.inv.p);
     }
     out.rows.alloc(slots ? slots : 4);
     if (slots)

@@ -1,16 +1,17 @@
-// Frequency-ranked row space for the lazy engine's visited bitmaps (a B200 layout choice;
-// the reference tests V_curr/V_next by plain row id, R:src/bfs_engine.cpp:286-289).
+// Hot-row view for the lazy engine's visited bitmaps (a B200 layout choice; the reference
+// tests V_curr/V_next by plain row id, R:src/bfs_engine.cpp:286-289).
 //
 // Stage 1 is bound by its visited tests: one random 4-byte load per candidate row into a
 // 2 MB bitmap (C2), served from L1 or L2. The tests concentrate on few rows — on Kron-20
 // (Jaccard order) the 10 % most frequent rows take 86 % of them — but those rows are
 // scattered over the id space, so every hot bit drags a 128 B L1 line of cold neighbours.
-// σ ranks the rows by their BVSS slot count (most frequent first, ties by id): in σ space
-// the hot rows' bits are contiguous, the hottest ~2 M of them in the first ~256 KB — what
-// one SM's L1 holds. The lazy kernel keeps V_curr / V_next in σ space and reads an engine
-// copy of row_ids holding σ(row); stage 2 maps each discovery back (σ⁻¹) to store its
-// level and set its bit in the original-space frontier bitmap (α of the slice sets, the
-// next queue).
+// The view ranks the rows by BVSS slot count and gives the K most frequent (K ≈ 1 M: 128 KB
+// of bits) engine ids 0..K-1 — a dense hot prefix of the visited bitmaps that L1 keeps —
+// while every other row r keeps its place at engine id 32·hot_words + r. An engine copy
+// of row_ids holds the engine ids. Stage 2 sweeps the hot prefix first (each discovery
+// mapped back by σ⁻¹ to store its level and RED its bit into the original-space frontier
+// Fd), then the row words exactly like the plain engine, merging Fd — so only hot
+// discoveries (≤ K per BFS) pay a scattered update.
 //
 // The canonical BVSS arrays are untouched (API, parity, eager engine).
 #pragma once
@@ -20,11 +21,14 @@
 namespace blestgpu {
 
 struct SigmaView {
-    DevBuf<uint32_t> rows;  // engine row_ids: σ(row); padding slots keep row n
-    DevBuf<uint32_t> sig;   // row -> σ(row)
-    DevBuf<uint32_t> inv;   // σ -> row
+    uint32_t K = 0;          // hot rows
+    uint64_t hot_words = 0;  // hot prefix of the visited bitmaps, words (multiple of 4)
+    DevBuf<uint32_t> rows;   // engine row_ids (hot rank, or 32·hot_words + row); padding kept
+    DevBuf<uint32_t> sig;    // row -> engine id
+    DevBuf<uint32_t> inv;    // hot rank -> row
 };
 
-void sigma_view_build(const DeviceBvss& b, SigmaView& out);
+// hot_cap: most hot rows (0 = default 2^20).
+void sigma_view_build(const DeviceBvss& b, SigmaView& out, uint32_t hot_cap = 0);
 
 }  // namespace blestgpu
