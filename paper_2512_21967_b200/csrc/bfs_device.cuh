@@ -11,7 +11,11 @@ namespace bfsdev {
 #ifndef BLEST_KBATCH
 #define BLEST_KBATCH 4
 #endif
-constexpr int kBatch = BLEST_KBATCH;  // VSSs in flight per warp
+#ifndef BLEST_KBATCH_LAZY
+#define BLEST_KBATCH_LAZY 3
+#endif
+constexpr int kBatch = BLEST_KBATCH;           // eager: VSSs in flight per warp
+constexpr int kBatchLazy = BLEST_KBATCH_LAZY;  // lazy (C2: 3 → 1.73 ms, 4 → 1.87, 2 → 2.03)
 constexpr int kPushCap = 64;      // per-warp push buffer entries (eager)
 constexpr unsigned long long kNoEntry = ~0ull;
 
@@ -170,7 +174,7 @@ __device__ __forceinline__ unsigned long long block_excl_scan(Smem<THREADS, MODE
 // Warp flush (eager): reserve room for the buffered slice sets' VSS ranges with one
 // atomicAdd and write the expanded entries. Returns VSS entries written.
 __device__ __forceinline__ uint32_t flush_pushes(const Params& p, unsigned long long* buf, uint32_t& count,
-                                 unsigned long long* Qn, unsigned long long* qlen_next) {
+                                 unsigned long long* Qn, unsigned long long* qlen_next, bool pf) {
     const unsigned lane = lane_id();
     uint32_t total = 0;
     uint32_t my_off[kPushCap / 32], my_b[kPushCap / 32], my_len[kPushCap / 32];
@@ -204,7 +208,15 @@ __device__ __forceinline__ uint32_t flush_pushes(const Params& p, unsigned long 
                 len = __shfl_sync(0xffffffffu, my_len[kk], src_lane);
             }
         const unsigned long long aux = buf[i] & 0xFFFFFFFF00000000ull;
-        for (uint32_t t = lane; t < len; t += 32) Qn[base + off + t] = aux | (unsigned long long)(b + t);
+        for (uint32_t t = lane; t < len; t += 32) {
+            Qn[base + off + t] = aux | (unsigned long long)(b + t);
+            if (pf) {  // sparse level: pull the next level's VSS lines into L2
+                const uint64_t v = b + t;
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.masks + 32 * v));
+#pragma unroll
+                for (int l = 0; l < 4; ++l) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.rows4 + 32 * v + 8 * l));
+            }
+        }
     }
     __syncwarp();
     count = 0;
@@ -215,12 +227,12 @@ __device__ __forceinline__ uint32_t flush_pushes(const Params& p, unsigned long 
 __device__ __forceinline__ void push_column(const Params& p, bool flag, unsigned long long item,
                                             unsigned long long* buf, uint32_t& count,
                                             unsigned long long* Qn, unsigned long long* qlen_next,
-                                            uint32_t& pushes, uint32_t& full) {
+                                            uint32_t& pushes, uint32_t& full, bool pf) {
     const unsigned ball = __ballot_sync(0xffffffffu, flag);
     if (!ball) return;
     const uint32_t k = __popc(ball);
     if (count + k > kPushCap) {
-        const uint32_t t = flush_pushes(p, buf, count, Qn, qlen_next);
+        const uint32_t t = flush_pushes(p, buf, count, Qn, qlen_next, pf);
         if (lane_id() == 0) {  // per-warp quantities: count once, not per lane
             pushes += t;
             full += 1;

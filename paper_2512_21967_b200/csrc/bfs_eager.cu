@@ -202,13 +202,13 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                         const uint32_t x = row_of(rw, k);
                         const bool push = ((disc >> k) & 1u) && ((vw[k] >> (8 * ((x >> 3) & 3))) & 0xFFu) == 0;
                         push_column(p, push, (unsigned long long)(x >> 3) << 32 | (x >> 3), pbuf, pcount, Qn,
-                                    qlen_next, ctr[3], ctr[1]);
+                                    qlen_next, ctr[3], ctr[1], !recheck);
                     }
                 }
             }
         }
         if (pcount) {
-            const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next);
+            const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next, !recheck);
             if (lane == 0) {
                 ctr[3] += t;
                 ctr[1] += 1;
@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
         if (zss != 0xFFFFFFFFu) Fz[zss] = 0;
         for (uint64_t i = gtid + gthreads; i < prev_len; i += gthreads) Fz[Qz[i] >> 32] = 0;
         prev_len = len;
+        if ((p.xflags & 64) && threadIdx.x == 0 && level - 1 < p.trace_cap)  // timing study:
+            atomicMax(&p.tstamp[3ull * (level - 1) + 1], globaltimer());      // last CTA's pull end
         next_len = level_barrier(p, sm, gen, level, ctr, 2, qlen_next);
     }
     if (gtid == 0) p.ctl[4] = level - 1;

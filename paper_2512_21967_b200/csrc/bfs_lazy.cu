@@ -2,7 +2,7 @@
 // persistent cooperative kernel.
 //
 // Stage 1 (pull, :273-292). Warps take queue positions round-robin exactly like the
-// reference (p ≡ warp mod #warps, :190), kBatch at a time, so neighbouring warps stream
+// reference (p ≡ warp mod #warps, :190), kBatchLazy at a time, so neighbouring warps stream
 // neighbouring VSSs. Queue entries carry the set's frontier byte α (final when stage 2
 // enqueued it). Per VSS: one coalesced 128 B mask line and four 128 B row-id lines
 // (streaming loads), AND with α, and for every nonzero column the visited test: V_curr
@@ -29,7 +29,7 @@ using namespace bfsdev;
 #ifndef BLEST_MINB
 #define BLEST_MINB 1
 #endif
-// Visited tests of one batch (kBatch VSSs × 4 columns per lane) in batch-wide phases,
+// Visited tests of one batch (kBatchLazy VSSs × 4 columns per lane) in batch-wide phases,
 // each phase's memory operations in flight together (one latency per phase, not one per
 // VSS): (A) for every column with a nonzero pull, the row's word of the test bitmap W —
 // a plain, L1-cached load; (B) optionally (Params::recheck) the words still clear re-read
@@ -47,9 +47,9 @@ using namespace bfsdev;
 template <int PULL, typename Rows, typename Mask>
 __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t* W, uint32_t* Vn, bool recheck,
                                                 unsigned long long e, Rows rows, Mask mask) {
-    uint32_t vw[4 * kBatch];
+    uint32_t vw[4 * kBatchLazy];
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
+    for (int j = 0; j < kBatchLazy; ++j) {
         const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
         const uint4 r = rows(j);
         const uint32_t u[4] = {r.x, r.y, r.z, r.w};
@@ -77,7 +77,7 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
     }
     if (recheck) {
 #pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
+        for (int j = 0; j < kBatchLazy; ++j) {
             const uint4 r = rows(j);
             const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -86,7 +86,7 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
     }
     uint32_t reds = 0;
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
+    for (int j = 0; j < kBatchLazy; ++j) {
         const uint4 r = rows(j);
         const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -204,21 +204,21 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
             const uint64_t qstride = NW, q0 = gw, qend = len;
             const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
             const uint32_t* W = recheck ? Vc : Vn;
-            const uint64_t step = qstride * kBatch;
+            const uint64_t step = qstride * kBatchLazy;
             auto qload = [&](uint64_t base) -> unsigned long long {
                 const uint64_t pos = base + (uint64_t)lane * qstride;
-                return (lane < kBatch && pos < qend) ? Qc[pos] : kNoEntry;
+                return (lane < kBatchLazy && pos < qend) ? Qc[pos] : kNoEntry;
             };
-            // Register batches: kBatch VSSs' mask words and row ids loaded together (streaming
+            // Register batches: kBatchLazy VSSs' mask words and row ids loaded together (streaming
             // loads), queue entries of the next batch fetched while this batch is processed.
             unsigned long long e_next = qload(q0);
             for (uint64_t p0 = q0; p0 < qend; p0 += step) {
                 const unsigned long long e = e_next;
                 e_next = qload(p0 + step);
-                uint32_t mk[kBatch];
-                uint4 rw[kBatch];
+                uint32_t mk[kBatchLazy];
+                uint4 rw[kBatchLazy];
 #pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
+                for (int j = 0; j < kBatchLazy; ++j) {
                     const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
                     const bool ok = ej != kNoEntry;
                     const uint64_t v = ok ? (uint32_t)ej : 0u;
