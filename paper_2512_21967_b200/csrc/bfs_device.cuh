@@ -275,8 +275,10 @@ __device__ __forceinline__ void column_counts(uint32_t m, uint32_t alpha, uint32
     }
 }
 
-// Flush per-thread counters into the CTA's shared counters, then (thread 0) into the
-// level's trace row; then the grid barrier; block 0 stamps the time.
+// Flush per-thread counters into the CTA's shared counters, the grid barrier, then
+// (thread 0) the CTA's counters into the level's trace row; block 0 stamps the time. The
+// trace atomics follow the barrier so its fence never waits on them (one L2 round trip
+// less per level; they land before the kernel ends, and row `level` is not reset again).
 template <int THREADS, int MODE>
 __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS, MODE>& sm, unsigned& gen,
                                                   uint32_t level, uint32_t (&c)[4], int stamp_slot,
@@ -288,20 +290,26 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
         c[i] = 0;
     }
     __syncthreads();
+    unsigned long long mine[4] = {0, 0, 0, 0};
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            mine[i] = sm.ctr[i];
+            sm.ctr[i] = 0;
+        }
+    }
+    const uint32_t pay = grid_barrier_pay(p.bar, gen, payload);
     if (threadIdx.x == 0) {
         const uint32_t row = min(level - 1, p.trace_cap - 1);
         unsigned long long* t = p.trace + 8ull * row;
-        if (sm.ctr[0]) {
-            atomicAdd(&t[3], sm.ctr[0]);
+        if (mine[0]) {
+            atomicAdd(&t[3], mine[0]);
             atomicMax(&p.ctl[5], (unsigned long long)level);
         }
-        if (sm.ctr[1]) atomicAdd(&t[4], sm.ctr[1]);
-        if (sm.ctr[2]) atomicAdd(&t[6], sm.ctr[2]);
-        if (sm.ctr[3]) atomicAdd(&t[7], sm.ctr[3]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sm.ctr[i] = 0;
+        if (mine[1]) atomicAdd(&t[4], mine[1]);
+        if (mine[2]) atomicAdd(&t[6], mine[2]);
+        if (mine[3]) atomicAdd(&t[7], mine[3]);
     }
-    const uint32_t pay = grid_barrier_pay(p.bar, gen, payload);
     if (blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
         p.tstamp[3ull * (level - 1) + stamp_slot] = globaltimer();
     return pay;
@@ -540,9 +548,10 @@ __device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
     uint32_t* Fd = p.B2;
-    const uint64_t gtid = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
-    const uint64_t gthreads = (uint64_t)gridDim.x * THREADS;
-    for (uint64_t w = gtid; w < p.hot_words; w += gthreads) {
+    // word w goes to CTA w mod G: the dense, hottest words (most of the early levels'
+    // discoveries) spread over every CTA instead of the first hot_words / THREADS ones
+    for (uint64_t w = blockIdx.x + (uint64_t)threadIdx.x * gridDim.x; w < p.hot_words;
+         w += (uint64_t)THREADS * gridDim.x) {
         const uint32_t nx = __ldcg(Vn + w), d = nx & ~Vc[w];
         if (!d) continue;
         Vc[w] = nx;
