@@ -52,6 +52,12 @@ CONFIGS = {
 }
 
 
+def coll_dev():
+    """Device for the small bookkeeping collectives: CUDA under NCCL, host under gloo."""
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -212,15 +218,24 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    if args.impl == "reference" and rank != 0:
-        return  # the reference arm runs on rank 0 only
+    if args.impl == "reference":
+        if rank != 0:
+            return  # the reference arm runs on rank 0 only, the other ranks exit without work
+        world = 1  # ... and without a process group (nobody else would join it)
 
     import torch
     import torch.distributed as dist
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL over NVLink, one GPU per rank. BLEST_DIST_BACKEND=gloo lets several ranks share
+        # one GPU (local % device_count) to exercise this path on a single-GPU box.
+        backend = os.environ.get("BLEST_DIST_BACKEND", "nccl")
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     import paper_2512_21967_b200 as B
@@ -244,7 +259,9 @@ def main():
     workload = dict(workload=args.config, graph=prep["desc"], n=n, arcs=int(b.m),
                     num_vss=int(b.num_vss), ordering=plan.strategy.value, engine=mode.value,
                     pull=args.pull, prepass=args.prepass, postpass=args.postpass, sources=len(mine) * world, source_seed=args.source_seed,
-                    l2="inputs larger than L2 (BVSS %.2f GB > 126 MB), no flush" % (b.num_vss * 644 / 1e9),
+                    l2=("inputs larger than L2 (BVSS %.2f GB > 126 MB), no flush" % (b.num_vss * 644 / 1e9)
+                        if b.num_vss * 644 >= 2 * 126e6 else
+                        "BVSS %.1f MB fits in L2: 512 MB L2 flush before every timed BFS" % (b.num_vss * 644 / 1e6)),
                     prep_s=prep["times"], parallelism=f"source-sharded x{world}" if world > 1 else "1 GPU")
 
     if args.partition == "rows" or args.virtual_ranks:
@@ -291,16 +308,23 @@ def main():
     for s in warm:
         L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), None, C.byref(ctr), None, 0))
     # ---- timed region: K fused launches, CUDA events on the launching stream ----
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(mine) + 1)]
+    # Structures smaller than 2x the 126 MB L2 (C1) get an L2 flush (a 512 MB write) before
+    # every timed BFS, outside its event pair; larger ones stream from HBM anyway.
+    flush = b.num_vss * 644 < 2 * 126e6
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush else None
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(len(mine))]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(len(mine))]
     launches0 = lib.blest_kernel_launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ev[0].record(stream)
         for k, s in enumerate(mine):
+            if flush:
+                scratch.fill_(k & 0xFF)
+            ev_s[k].record(stream)
             L.check(lib.blest_bfs_launch(b.handle, int(s), C.byref(ecfg)))
-            ev[k + 1].record(stream)
+            ev_e[k].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -308,7 +332,7 @@ def main():
     g_ctas, g_thr = C.c_uint32(), C.c_uint32()
     L.check(lib.blest_bfs_last_geometry(b.handle, C.byref(g_ctas), C.byref(g_thr)))
     L.check(lib.blest_bfs_finish(b.handle, None, C.byref(ctr), None, 0))
-    t = np.array([ev[k].elapsed_time(ev[k + 1]) / 1e3 for k in range(len(mine))])
+    t = np.array([ev_s[k].elapsed_time(ev_e[k]) / 1e3 for k in range(len(mine))])
     E = np.array([c["E"] for c in census], np.float64)
     hm = len(t) / float(np.sum(t / E)) / 1e9
     total_s = float(t.sum())
@@ -317,7 +341,7 @@ def main():
     peak, peak_kind = load_peaks()
     value, elapsed = hm, total_s
     if world > 1:
-        tt = torch.tensor([hm, total_s], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([hm, total_s], dtype=torch.float64, device=coll_dev())
         allv = [torch.zeros_like(tt) for _ in range(world)]
         dist.all_gather(allv, tt)
         value = float(sum(x[0].item() for x in allv))
@@ -412,7 +436,7 @@ def run_partitioned(args, prep, B, L, lib, srcs_orig, perm, world, rank, local, 
         part = GpuPartition(gp, lo, hi, words_per_rank(n, G))
         bfs = RowPartitionedBfs(part, n, nccl_allgather())
         run = lambda s: bfs.run(int(s))
-        mode = f"rows x{G} ranks, NCCL all-gather per level"
+        mode = f"rows x{G} ranks, {dist.get_backend().upper()} all-gather per level"
     del prep["b"]  # the single-GPU structure is not used by this mode
     for s in srcs[: args.warmup]:
         run(s)
@@ -434,7 +458,7 @@ def run_partitioned(args, prep, B, L, lib, srcs_orig, perm, world, rank, local, 
             reached = r.levels != 0xFFFFFFFF
             e = int(deg[r.row_lo:r.row_hi][reached].sum())
         if world > 1 and not args.virtual_ranks:
-            tt = torch.tensor([t, float(e)], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([t, float(e)], dtype=torch.float64, device=coll_dev())
             tmax = tt.clone()
             dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
             dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)

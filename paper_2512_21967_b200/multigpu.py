@@ -126,9 +126,15 @@ def nccl_allgather(group=None):
 
     def gather(local):
         world = dist.get_world_size(group)
-        out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
-        dist.all_gather_into_tensor(out, local, group=group)
-        return out
+        if dist.get_backend(group) == "nccl":
+            out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+            dist.all_gather_into_tensor(out, local, group=group)
+            return out
+        # gloo (several ranks sharing one GPU in tests): through host memory
+        host = local.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        return torch.cat(parts).to(local.device)
     return gather
 
 
