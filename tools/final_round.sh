@@ -11,3 +11,4 @@ timeout 600 python tools/phase_profile.py --config c2 --sources 2 > gpurun_out/f
 timeout 600 python tools/phase_profile.py --config c3 --sources 1 > gpurun_out/final/phase_c3.txt 2>&1
 timeout 1200 bash tools/profile.sh c2 > gpurun_out/final/profile_c2.log 2>&1
 timeout 1200 bash tools/profile.sh c3 > gpurun_out/final/profile_c3.log 2>&1
+timeout 1800 python bench.py --config c5 --steps 4 --warmup 1 --no-cpu-baseline > gpurun_out/final/bench_c5.json 2> gpurun_out/final/bench_c5.err
