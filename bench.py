@@ -195,7 +195,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="auto", choices=["auto", "eager", "lazy"])
+    ap.add_argument("--mode", default="b200", choices=["b200", "auto", "eager", "lazy"],
+                    help="engine: b200 = lazy unless the graph is low-degree (arcs/n < 8, e.g. grids: "
+                         "many levels, where eager's one barrier per level wins); auto = the reference's "
+                         "rule (R:src/bfs_engine.cpp:358-362)")
     ap.add_argument("--pull", default="popc", choices=["popc", "mma"])
     ap.add_argument("--order", default=None, choices=["auto", "identity", "rcm", "jaccard", "random"])
     ap.add_argument("--window", type=int, default=1 << 16)
@@ -246,8 +249,11 @@ def main():
 
     prep = prepare(args.config, args.order, args.window, args.prepass, args.postpass)
     g, b, plan, perm = prep["g"], prep["b"], prep["plan"], prep["perm"]
-    cfg = B.EngineConfig(mode=B.engine_mode_from_string(args.mode), pull=args.pull)
-    mode = B.choose_mode(b, plan, cfg)
+    if args.mode == "b200":  # measured: lazy wins on Kron and urand (C3 2.7 vs 4.75 ms), eager on grids
+        mode = B.EngineMode.Lazy if b.m >= 8 * max(b.n, 1) else B.EngineMode.Eager
+    else:
+        cfg = B.EngineConfig(mode=B.engine_mode_from_string(args.mode), pull=args.pull)
+        mode = B.choose_mode(b, plan, cfg)
     lazy = mode == B.EngineMode.Lazy
     n = b.n
     total_sources = args.steps * world + args.warmup
@@ -257,7 +263,7 @@ def main():
     warm = srcs[: args.warmup]
     threads = os.cpu_count() or 1
     workload = dict(workload=args.config, graph=prep["desc"], n=n, arcs=int(b.m),
-                    num_vss=int(b.num_vss), ordering=plan.strategy.value, engine=mode.value,
+                    num_vss=int(b.num_vss), ordering=plan.strategy.value, engine=mode.value, engine_policy=args.mode,
                     pull=args.pull, prepass=args.prepass, postpass=args.postpass, sources=len(mine) * world, source_seed=args.source_seed,
                     l2=("inputs larger than L2 (BVSS %.2f GB > 126 MB), no flush" % (b.num_vss * 644 / 1e9)
                         if b.num_vss * 644 >= 2 * 126e6 else

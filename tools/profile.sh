@@ -5,7 +5,7 @@
 # Outputs in gpurun_out/; tools/summarize_profile.py turns them into profiles/*.
 set -e
 CFG=${1:-c2}
-MODE=${2:-auto}
+MODE=${2:-b200}
 OUT=gpurun_out
 mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_${CFG}.csv \
