@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
             break;
         }
         if (gtid == 0) {
+            p.ctl[7] = 0;  // stage-1 tail chunk counter (read after the expansion barrier)
             if (level - 1 < p.trace_cap) {
                 p.trace[8ull * (level - 1) + 0] = level;
                 p.trace[8ull * (level - 1) + 1] = len;
@@ -198,35 +199,50 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
             for (uint64_t w = gtid; w < p.words; w += gthreads) Fd[w] = 0;
         // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
         if (gw < NW) {
-            // Position walk: round-robin over all warps like the reference (p ≡ warp mod
-            // #warps, :190). (A CTA-contiguous walk, for L1 sharing among an SM's warps,
-            // measured no better.)
-            const uint64_t qstride = NW, q0 = gw, qend = len;
             const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
             const uint32_t* W = recheck ? Vc : Vn;
-            const uint64_t step = qstride * kBatchLazy;
-            auto qload = [&](uint64_t base) -> unsigned long long {
-                const uint64_t pos = base + (uint64_t)lane * qstride;
-                return (lane < kBatchLazy && pos < qend) ? Qc[pos] : kNoEntry;
-            };
-            // Register batches: kBatchLazy VSSs' mask words and row ids loaded together (streaming
-            // loads), queue entries of the next batch fetched while this batch is processed.
-            unsigned long long e_next = qload(q0);
-            for (uint64_t p0 = q0; p0 < qend; p0 += step) {
-                const unsigned long long e = e_next;
-                e_next = qload(p0 + step);
-                uint32_t mk[kBatchLazy];
-                uint4 rw[kBatchLazy];
+            // Batches of kBatchLazy queue positions q0, q0+qs, ... < qe: mask words and row
+            // ids loaded together (streaming loads), the next batch's queue entries fetched
+            // while this batch is processed.
+            auto run = [&](uint64_t q0, uint64_t qs, uint64_t qe) {
+                const uint64_t step = qs * kBatchLazy;
+                auto qload = [&](uint64_t base) -> unsigned long long {
+                    const uint64_t pos = base + (uint64_t)lane * qs;
+                    return (lane < kBatchLazy && pos < qe) ? Qc[pos] : kNoEntry;
+                };
+                unsigned long long e_next = qload(q0);
+                for (uint64_t p0 = q0; p0 < qe; p0 += step) {
+                    const unsigned long long e = e_next;
+                    e_next = qload(p0 + step);
+                    uint32_t mk[kBatchLazy];
+                    uint4 rw[kBatchLazy];
 #pragma unroll
-                for (int j = 0; j < kBatchLazy; ++j) {
-                    const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
-                    const bool ok = ej != kNoEntry;
-                    const uint64_t v = ok ? (uint32_t)ej : 0u;
-                    mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
-                    rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
+                    for (int j = 0; j < kBatchLazy; ++j) {
+                        const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
+                        const bool ok = ej != kNoEntry;
+                        const uint64_t v = ok ? (uint32_t)ej : 0u;
+                        mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
+                        rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
+                    }
+                    ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
+                                                [&](int j) { return mk[j]; });
                 }
-                ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
-                                            [&](int j) { return mk[j]; });
+            };
+            // Positions [0, len - tail): round-robin over the warps like the reference
+            // (p ≡ warp mod #warps, :190). The last eighth (dense levels, whole grid) is
+            // handed out in chunks of 32 consecutive positions from a counter, so warps that
+            // finish early absorb the tail instead of waiting at the barrier.
+            const uint64_t tail = (NW == all_warps && len >= p.dense_min && !(p.xflags & 2048)) ? len / 8 : 0;
+            const uint64_t stat = len - tail;
+            run(gw, NW, stat);
+            if (tail) {
+                for (;;) {
+                    unsigned long long c = 0;
+                    if (lane == 0) c = atomicAdd(&p.ctl[7], 32ull);
+                    c = __shfl_sync(0xffffffffu, c, 0);
+                    if (c >= tail) break;
+                    run(stat + c, 1, stat + min(c + 32, (unsigned long long)tail));
+                }
             }
         }
         level_barrier(p, sm, gen, level, ctr, 1);
