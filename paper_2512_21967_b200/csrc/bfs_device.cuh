@@ -52,6 +52,7 @@ struct Params {
     uint64_t hot_words;
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
     uint32_t lazy_recheck;  // lazy: test V_curr and re-check V_next at L2 (BLEST_LAZY_RECHECK)
+    uint32_t tail_div;      // lazy: dense levels hand out their last 1/tail_div dynamically (0 = off)
 };
 
 template <int THREADS, int MODE = 0>

@@ -229,10 +229,10 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                 }
             };
             // Positions [0, len - tail): round-robin over the warps like the reference
-            // (p ≡ warp mod #warps, :190). The last eighth (dense levels, whole grid) is
+            // (p ≡ warp mod #warps, :190). The last 1/tail_div (8; dense levels, whole grid) is
             // handed out in chunks of 32 consecutive positions from a counter, so warps that
             // finish early absorb the tail instead of waiting at the barrier.
-            const uint64_t tail = (NW == all_warps && len >= p.dense_min && !(p.xflags & 2048)) ? len / 8 : 0;
+            const uint64_t tail = (NW == all_warps && len >= p.dense_min && p.tail_div) ? len / p.tail_div : 0;
             const uint64_t stat = len - tail;
             run(gw, NW, stat);
             if (tail) {
