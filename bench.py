@@ -355,11 +355,12 @@ def main():
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----
     # blest_bfs_batch: the public many-sources call; source k's full level array is copied
-    # to pinned host memory while source k+1 runs. Chunks of as many sources as 8 GB of
-    # pinned level arrays hold (C2: all 64); each source's time = its chunk's wall time / size.
+    # to pinned host memory while source k+1 runs. Chunks of <= 16 sources (one pinned
+    # buffer, reused; a 64-source / 4.3 GB buffer measured slower D2H: e2e 141 -> 74 GTEPS);
+    # each source's time = its chunk's wall time / size.
     e2e = None
     if not args.no_e2e:
-        chunk = max(1, min(len(mine), int(8e9 // (4 * max(n, 1)))))  # <= 8 GB of pinned level arrays
+        chunk = max(1, min(16, len(mine), int(4e9 // (4 * max(n, 1)))))
         hl = torch.empty((chunk, n), dtype=torch.int32, pin_memory=True)
         hsrc = torch.empty(chunk, dtype=torch.int32, pin_memory=True)
         cbuf = (L.CountersT * chunk)()

@@ -321,3 +321,25 @@ def test_auto_pipeline_non_social(oracle, kind):
         assert np.array_equal(r.bfs.levels, oracle.reference_bfs(csr, int(src))[0]), (kind, int(src))
         if not plan.classification.is_social_like:  # the reference's auto rule (R:src/bfs_engine.cpp:358-362)
             assert r.chosen_mode == B.EngineMode.Eager
+
+
+def test_lazy_dense_levels_rmat18(oracle, monkeypatch):
+    """A graph big enough for dense levels (queue ≥ 8 VSSs per warp): the lazy engine's
+    dynamic tail hand-out and the hot-row view run unforced; levels and counters equal the
+    oracle's, and a hot-prefix cap of 4096 rows (most hubs outside the prefix) agrees too."""
+    g = B.Graph.generate_rmat(18, 16, 2)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    srcs = g.pick_sources(2, 5)
+    want, _ = oracle.reference_bfs_many(csr, srcs)
+    ob = oracle.build_bvss(csr)
+    for hot in (None, "4096"):
+        if hot:
+            monkeypatch.setenv("BLEST_HOT", hot)
+        b = B.build_bvss(g)  # a fresh structure builds its hot view under the current cap
+        for k, s in enumerate(srcs):
+            res, cnt = B.run_lazy(b, int(s))
+            assert np.array_equal(res.levels, want[k]), (hot, int(s))
+            o_eng = oracle.run_engine(ob, int(s), True)
+            assert cnt.vss_dequeues == o_eng.counters["vss_dequeues"]
+            assert max(t.queue_size for t in cnt.trace) >= 296 * 16 * 8  # a dense level ran (dense_min)
