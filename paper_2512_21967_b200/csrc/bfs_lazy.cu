@@ -29,9 +29,6 @@ using namespace bfsdev;
 #ifndef BLEST_MINB
 #define BLEST_MINB 1
 #endif
-#ifndef BLEST_LAZY_PIPE2
-#define BLEST_LAZY_PIPE2 0
-#endif
 // Visited tests of one batch (kBatchLazy VSSs × 4 columns per lane) in batch-wide phases,
 // each phase's memory operations in flight together (one latency per phase, not one per
 // VSS): (A) for every column with a nonzero pull, the row's word of the test bitmap W —
@@ -99,7 +96,10 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
 }
 
 template <int PULL, int THREADS, bool SIGMA>
-__global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)) k_bfs_lazy(Params p) {
+#ifndef BLEST_LAZY_MINB
+#define BLEST_LAZY_MINB (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)
+#endif
+__global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
     const unsigned lane = lane_id();
@@ -213,39 +213,6 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                     const uint64_t pos = base + (uint64_t)lane * qs;
                     return (lane < kBatchLazy && pos < qe) ? Qc[pos] : kNoEntry;
                 };
-#if BLEST_LAZY_PIPE2
-                // software pipeline: batch i+1's mask words / row ids are in flight while
-                // batch i's visited tests run (the stream otherwise idles during the tests)
-                auto sload = [&](unsigned long long e, uint32_t (&mk)[kBatchLazy], uint4 (&rw)[kBatchLazy]) {
-#pragma unroll
-                    for (int j = 0; j < kBatchLazy; ++j) {
-                        const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
-                        const bool ok = ej != kNoEntry;
-                        const uint64_t v = ok ? (uint32_t)ej : 0u;
-                        mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
-                        rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
-                    }
-                };
-                unsigned long long e_cur = qload(q0), e_nxt = qload(q0 + step);
-                uint32_t mk[kBatchLazy];
-                uint4 rw[kBatchLazy];
-                sload(e_cur, mk, rw);
-                for (uint64_t p0 = q0; p0 < qe; p0 += step) {
-                    const unsigned long long e_nn = qload(p0 + 2 * step);
-                    uint32_t mk2[kBatchLazy];
-                    uint4 rw2[kBatchLazy];
-                    sload(e_nxt, mk2, rw2);
-                    ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e_cur, [&](int j) { return rw[j]; },
-                                                [&](int j) { return mk[j]; });
-#pragma unroll
-                    for (int j = 0; j < kBatchLazy; ++j) {
-                        mk[j] = mk2[j];
-                        rw[j] = rw2[j];
-                    }
-                    e_cur = e_nxt;
-                    e_nxt = e_nn;
-                }
-#else
                 unsigned long long e_next = qload(q0);
                 for (uint64_t p0 = q0; p0 < qe; p0 += step) {
                     const unsigned long long e = e_next;
@@ -263,7 +230,6 @@ __global__ void __launch_bounds__(THREADS, (BLEST_MINB > 1 ? BLEST_MINB : 1024 /
                     ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
                                                 [&](int j) { return mk[j]; });
                 }
-#endif
             };
             // Positions [0, len - tail): round-robin over the warps like the reference
             // (p ≡ warp mod #warps, :190). The last 1/tail_div (8; dense levels, whole grid) is
