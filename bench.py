@@ -71,34 +71,43 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 20 ms from before the timed region
+    (nvidia-smi needs ~0.1 s to start); summary() keeps the samples read while the timed
+    region ran (mark()/unmark() bracket it), or the nearest ones when it was shorter."""
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (host time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except FileNotFoundError:
             self.proc = None
         return self
 
+    def mark(self):
+        self.t0 = time.time()
+
+    def unmark(self):
+        self.t1 = time.time()
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
 
-    def __exit__(self, *exc):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -107,14 +116,23 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        if self.t0 is not None and self.t1 is not None and rows:
+            inside = [r for t, r in rows if self.t0 <= t <= self.t1 + 0.05]
+            if not inside:  # region shorter than the sampling period: the nearest samples
+                mid = 0.5 * (self.t0 + self.t1)
+                inside = [r for t, r in sorted(rows, key=lambda tr: abs(tr[0] - mid))[:3]]
+            rows = inside
+        else:
+            rows = [r for _, r in rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def prepare(config: str, ordering_override: str | None, window: int, prepass: str = "none",
@@ -310,7 +328,8 @@ def main():
             L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), lv.ctypes.data, C.byref(ctr), None, 0))
             assert np.array_equal(lv, want[k]), f"levels mismatch for source {int(s)}"
         log(f"validated {len(chk)} sources bit-exact against the CPU oracle")
-    # ---- warmup ----
+    # ---- warmup (the clock sampler starts here so it is running in the timed region) ----
+    clk = ClockSampler(local).start()
     for s in warm:
         L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), None, C.byref(ctr), None, 0))
     # ---- timed region: K fused launches, CUDA events on the launching stream ----
@@ -324,14 +343,16 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for k, s in enumerate(mine):
-            if flush:
-                scratch.fill_(k & 0xFF)
-            ev_s[k].record(stream)
-            L.check(lib.blest_bfs_launch(b.handle, int(s), C.byref(ecfg)))
-            ev_e[k].record(stream)
-        torch.cuda.synchronize()
+    clk.mark()
+    for k, s in enumerate(mine):
+        if flush:
+            scratch.fill_(k & 0xFF)
+        ev_s[k].record(stream)
+        L.check(lib.blest_bfs_launch(b.handle, int(s), C.byref(ecfg)))
+        ev_e[k].record(stream)
+    torch.cuda.synchronize()
+    clk.unmark()
+    clk.stop()
     if world > 1:
         dist.barrier()
     launches = lib.blest_kernel_launches() - launches0
