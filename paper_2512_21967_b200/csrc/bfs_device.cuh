@@ -409,10 +409,11 @@ __device__ __forceinline__ void s2_load(const Params& p, const uint32_t* src, ui
 template <int THREADS>
 __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm, uint32_t level, uint32_t (&ctr)[4],
                                            uint64_t k0, uint64_t k1, bool single, const uint32_t (&keep)[4],
-                                           unsigned long long my_vss, unsigned long long my_sets) {
+                                           unsigned long long my_vss, unsigned long long my_sets,
+                                           const uint32_t* Fd) {
     constexpr unsigned long long kTagMask = (1ull << 40) - 1;
     constexpr uint64_t CH = 4ull * THREADS;
-    const uint32_t* Fd = p.B2;
+    // Fd: the frontier words being built this level (parameter)
     unsigned long long cta_vss = 0, cta_sets = 0;
     block_excl_scan(sm, my_vss, &cta_vss);
     block_excl_scan(sm, my_sets, &cta_sets);
@@ -481,14 +482,14 @@ __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm
 // hot_stage2), which are merged into the frontier words; their levels are already stored.
 template <int THREADS, bool HOT = false>
 __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
-                                            uint32_t (&ctr)[4]) {
+                                            uint32_t (&ctr)[4], uint32_t* Fd_out = nullptr) {
     constexpr unsigned long long kTagMask = (1ull << 40) - 1;
     constexpr uint64_t CH = 4ull * THREADS;
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     uint32_t* Vc = p.B0 + (HOT ? p.hot_words : 0);  // 16-byte aligned: hot_words % 4 == 0
     uint32_t* Vn = p.B1 + (HOT ? p.hot_words : 0);
-    uint32_t* Fd = p.B2;
+    uint32_t* Fd = Fd_out ? Fd_out : p.B2;  // the next level's frontier words
     const uint64_t chunks = (p.words + CH - 1) / CH;
     const uint64_t k0 = (uint64_t)blockIdx.x * chunks / gridDim.x, k1 = (uint64_t)(blockIdx.x + 1) * chunks / gridDim.x;
     const bool single = k1 - k0 <= 1;
@@ -536,7 +537,7 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
             }
         }
     }
-    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets);
+    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets, Fd);
 }
 
 // Hot-row stage 2 (sigma.cuh): the hot prefix of the visited bitmaps (hot_words words,
@@ -545,10 +546,9 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
 // a grid barrier; then lazy_stage2<HOT> sweeps the row words and merges Fd.
 template <int THREADS>
 __device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
-                                                uint32_t (&ctr)[4], unsigned& gen) {
+                                                uint32_t (&ctr)[4], unsigned& gen, uint32_t* Fd) {
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
-    uint32_t* Fd = p.B2;
     // word w goes to CTA w mod G: the dense, hottest words (most of the early levels'
     // discoveries) spread over every CTA instead of the first hot_words / THREADS ones
     for (uint64_t w = blockIdx.x + (uint64_t)threadIdx.x * gridDim.x; w < p.hot_words;
@@ -580,7 +580,7 @@ __device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1
     grid_barrier(p.bar, gen);  // the hot discoveries are in Fd
     if ((p.xflags & 32) && blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
         p.tstamp[3ull * (level - 1) + 1] = globaltimer();  // timing study: hot pass end
-    lazy_stage2<THREADS, true>(p, sm, level, ctr);
+    lazy_stage2<THREADS, true>(p, sm, level, ctr, Fd);
 }
 
 }  // namespace bfsdev

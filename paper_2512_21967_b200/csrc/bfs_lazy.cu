@@ -114,7 +114,6 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
     if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
     uint32_t* Vc = p.B0;
     uint32_t* Vn = p.B1;
-    uint32_t* Fd = p.B2;
     const uint4* __restrict__ rows4 = p.rows4;  // SIGMA: the σ view's row ids
 
     // ---- init_state (R:src/bfs_engine.cpp:30-49), fused ----
@@ -131,7 +130,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         const uint32_t seed = (w == vs_word) ? vs_bit : 0u;
         Vc[w] = seed;
         Vn[w] = seed;
-        if (w < p.words) Fd[w] = (w == src_word) ? src_bit : 0u;  // α of the source's set, level 1
+        if (w < p.words) p.B2[w] = (w == src_word) ? src_bit : 0u;  // α of the source's set, level 1
     }
     if (threadIdx.x == 0) {
         p.agg[blockIdx.x] = 0;
@@ -169,91 +168,127 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
                 for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
         }
         unsigned long long* Qc = p.Q0;
-        // ---- expand SL into the queue: equal contiguous share per warp ----
-        {
-            const uint64_t lo = (uint64_t)gw * len / all_warps, hi = (uint64_t)(gw + 1) * len / all_warps;
-            if (lo < hi) {
-                const uint8_t* Fd8 = reinterpret_cast<const uint8_t*>(Fd);
-                SetWindow win;
-                load_window(p, Fd8, find_set(p, S, lo), S, len, win);
-                for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
-                    if (c0 + 31 >= win.wend && win.wend < len) {  // slide to the set holding c0
-                        const unsigned own = __ballot_sync(0xffffffffu, win.first <= c0);
-                        const uint32_t nb = (c0 >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
-                        load_window(p, Fd8, nb, S, len, win);
-                    }
-                    const uint64_t q = c0 + lane;
-                    int l = 0;
+        // the level's frontier words (α) and the next level's: B2/B3 alternate, so the next
+        // frontier can be cleared while this one is still being read (no barrier between)
+        const uint32_t* Fd = (level & 1) ? p.B2 : p.B3;
+        uint32_t* Fn = (level & 1) ? p.B3 : p.B2;
+        const uint8_t* Fd8 = reinterpret_cast<const uint8_t*>(Fd);
+        // queue entry (α << 32 | VSS) of position c0 + lane; `win` is slid forward as needed
+        auto entry_at = [&](uint64_t c0, SetWindow& win) -> unsigned long long {
+            if (c0 + 31 >= win.wend && win.wend < len) {  // slide to the set holding c0
+                const unsigned own = __ballot_sync(0xffffffffu, win.first <= c0);
+                const uint32_t nb = (c0 >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
+                load_window(p, Fd8, nb, S, len, win);
+            }
+            const uint64_t q = c0 + lane;
+            int l = 0;
 #pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const uint64_t f = __shfl_sync(0xffffffffu, win.first, l + step);
-                        if (f <= q) l += step;
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint64_t f = __shfl_sync(0xffffffffu, win.first, l + step);
+                if (f <= q) l += step;
+            }
+            const uint32_t v = __shfl_sync(0xffffffffu, win.b, l) +
+                               (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
+            const uint32_t a = __shfl_sync(0xffffffffu, win.alpha, l);
+            return ((unsigned long long)a << 32) | v;
+        };
+        const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
+        const uint32_t* W = recheck ? Vc : Vn;
+        // loads of the VSSs named by lanes 0..kBatchLazy-1 of e, then their visited tests
+        auto pull_batch = [&](unsigned long long e) {
+            uint32_t mk[kBatchLazy];
+            uint4 rw[kBatchLazy];
+#pragma unroll
+            for (int j = 0; j < kBatchLazy; ++j) {
+                const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
+                const bool ok = ej != kNoEntry;
+                const uint64_t v = ok ? (uint32_t)ej : 0u;
+                mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
+                rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
+            }
+            ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
+                                        [&](int j) { return mk[j]; });
+        };
+        if (len < p.dense_min) {
+            // ---- sparse level: every warp expands its own contiguous share of the queue
+            // and pulls it straight from registers — no materialised queue, no barrier ----
+            if (SIGMA)
+                for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
+            if (gw < NW) {
+                const uint64_t lo = (uint64_t)gw * len / NW, hi = (uint64_t)(gw + 1) * len / NW;
+                if (lo < hi) {
+                    SetWindow win;
+                    load_window(p, Fd8, find_set(p, S, lo), S, len, win);
+                    for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
+                        const unsigned long long mine = entry_at(c0, win);
+                        const uint32_t cnt = (hi - c0 < 32) ? (uint32_t)(hi - c0) : 32u;
+                        for (uint32_t k = 0; k < cnt; k += kBatchLazy) {
+                            unsigned long long e = __shfl_sync(0xffffffffu, mine, (lane + k) & 31);
+                            if (lane >= (uint32_t)kBatchLazy || k + lane >= cnt) e = kNoEntry;
+                            pull_batch(e);
+                        }
                     }
-                    const uint32_t v = __shfl_sync(0xffffffffu, win.b, l) +
-                                       (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
-                    const uint32_t a = __shfl_sync(0xffffffffu, win.alpha, l);
-                    if (q < hi) Qc[q] = ((unsigned long long)a << 32) | v;
                 }
             }
-        }
-        grid_barrier(p.bar, gen);
-
-        if (SIGMA)  // the expansion has read α: clear Fd for stage 2's scattered discoveries
-            for (uint64_t w = gtid; w < p.words; w += gthreads) Fd[w] = 0;
-        // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
-        if (gw < NW) {
-            const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
-            const uint32_t* W = recheck ? Vc : Vn;
-            // Batches of kBatchLazy queue positions q0, q0+qs, ... < qe: mask words and row
-            // ids loaded together (streaming loads), the next batch's queue entries fetched
-            // while this batch is processed.
-            auto run = [&](uint64_t q0, uint64_t qs, uint64_t qe) {
-                const uint64_t step = qs * kBatchLazy;
-                auto qload = [&](uint64_t base) -> unsigned long long {
-                    const uint64_t pos = base + (uint64_t)lane * qs;
-                    return (lane < kBatchLazy && pos < qe) ? Qc[pos] : kNoEntry;
-                };
-                unsigned long long e_next = qload(q0);
-                for (uint64_t p0 = q0; p0 < qe; p0 += step) {
-                    const unsigned long long e = e_next;
-                    e_next = qload(p0 + step);
-                    uint32_t mk[kBatchLazy];
-                    uint4 rw[kBatchLazy];
-#pragma unroll
-                    for (int j = 0; j < kBatchLazy; ++j) {
-                        const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
-                        const bool ok = ej != kNoEntry;
-                        const uint64_t v = ok ? (uint32_t)ej : 0u;
-                        mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
-                        rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
+        } else {
+            // ---- dense level: expand SL into the queue, equal contiguous share per warp ----
+            {
+                const uint64_t lo = (uint64_t)gw * len / all_warps, hi = (uint64_t)(gw + 1) * len / all_warps;
+                if (lo < hi) {
+                    SetWindow win;
+                    load_window(p, Fd8, find_set(p, S, lo), S, len, win);
+                    for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
+                        const unsigned long long e = entry_at(c0, win);
+                        if (c0 + lane < hi) Qc[c0 + lane] = e;
                     }
-                    ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
-                                                [&](int j) { return mk[j]; });
                 }
-            };
-            // Positions [0, len - tail): round-robin over the warps like the reference
-            // (p ≡ warp mod #warps, :190). The last 1/tail_div (8; dense levels, whole grid) is
-            // handed out in chunks of 32 consecutive positions from a counter, so warps that
-            // finish early absorb the tail instead of waiting at the barrier.
-            const uint64_t tail = (NW == all_warps && len >= p.dense_min && p.tail_div) ? len / p.tail_div : 0;
-            const uint64_t stat = len - tail;
-            run(gw, NW, stat);
-            if (tail) {
-                for (;;) {
-                    unsigned long long c = 0;
-                    if (lane == 0) c = atomicAdd(&p.ctl[7], 32ull);
-                    c = __shfl_sync(0xffffffffu, c, 0);
-                    if (c >= tail) break;
-                    run(stat + c, 1, stat + min(c + 32, (unsigned long long)tail));
+            }
+            if (SIGMA)  // Fn is the previous level's α: its readers finished long ago
+                for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
+            grid_barrier(p.bar, gen);
+
+            // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
+            if (gw < NW) {
+                // Batches of kBatchLazy queue positions q0, q0+qs, ... < qe: mask words and row
+                // ids loaded together (streaming loads), the next batch's queue entries fetched
+                // while this batch is processed.
+                auto run = [&](uint64_t q0, uint64_t qs, uint64_t qe) {
+                    const uint64_t step = qs * kBatchLazy;
+                    auto qload = [&](uint64_t base) -> unsigned long long {
+                        const uint64_t pos = base + (uint64_t)lane * qs;
+                        return (lane < kBatchLazy && pos < qe) ? Qc[pos] : kNoEntry;
+                    };
+                    unsigned long long e_next = qload(q0);
+                    for (uint64_t p0 = q0; p0 < qe; p0 += step) {
+                        const unsigned long long e = e_next;
+                        e_next = qload(p0 + step);
+                        pull_batch(e);
+                    }
+                };
+                // Positions [0, len - tail): round-robin over the warps like the reference
+                // (p ≡ warp mod #warps, :190). The last 1/tail_div (8; whole grid) is handed
+                // out in chunks of 32 consecutive positions from a counter, so warps that
+                // finish early absorb the tail instead of waiting at the barrier.
+                const uint64_t tail = (NW == all_warps && p.tail_div) ? len / p.tail_div : 0;
+                const uint64_t stat = len - tail;
+                run(gw, NW, stat);
+                if (tail) {
+                    for (;;) {
+                        unsigned long long c = 0;
+                        if (lane == 0) c = atomicAdd(&p.ctl[7], 32ull);
+                        c = __shfl_sync(0xffffffffu, c, 0);
+                        if (c >= tail) break;
+                        run(stat + c, 1, stat + min(c + 32, (unsigned long long)tail));
+                    }
                 }
             }
         }
         level_barrier(p, sm, gen, level, ctr, 1);
 
         if (SIGMA)
-            lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen);
+            lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen, Fn);
         else
-            lazy_stage2<THREADS>(p, sm, level, ctr);
+            lazy_stage2<THREADS>(p, sm, level, ctr, Fn);
         next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);
     }
     if (gtid == 0) p.ctl[4] = level - 1;
