@@ -249,8 +249,8 @@ def test_auto_pipeline_maps_levels_back(oracle):
     {},
     {"BLEST_SIGMA": "0"},                  # lazy: visited bitmaps by plain row id (no σ view)
     {"BLEST_LAZY_RECHECK": "1"},           # lazy: test V_curr, re-check V_next at L2
-    {"BLEST_DENSE_MIN": "1"},              # eager: F_next re-check on every level
-    {"BLEST_DENSE_MIN": "1000000000"},     # eager: never (straight to the atomic)
+    {"BLEST_DENSE_MIN": "1"},              # eager: F_next re-check on every level; lazy: queue + barrier on every level
+    {"BLEST_DENSE_MIN": "1000000000"},     # eager: never (straight to the atomic); lazy: every level expanded inside stage 1
 ])
 def test_engine_phase_variants(oracle, monkeypatch, env):
     """The batch-wide visited-test phases, the lazy σ view and their switches change only how
