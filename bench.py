@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="b200", choices=["b200", "auto", "eager", "lazy"],
                     help="engine: b200 = lazy unless the graph is low-degree (arcs/n < 8, e.g. grids: "
-                         "many levels, where eager's one barrier per level wins); auto = the reference's "
+                         "many levels, where eager's one barrier per level wins) or small (< 2^20 VSSs); auto = the reference's "
                          "rule (R:src/bfs_engine.cpp:358-362)")
     ap.add_argument("--pull", default="popc", choices=["popc", "mma"])
     ap.add_argument("--order", default=None, choices=["auto", "identity", "rcm", "jaccard", "random"])
@@ -267,8 +267,11 @@ def main():
 
     prep = prepare(args.config, args.order, args.window, args.prepass, args.postpass)
     g, b, plan, perm = prep["g"], prep["b"], prep["plan"], prep["perm"]
-    if args.mode == "b200":  # measured: lazy wins on Kron and urand (C3 2.7 vs 4.75 ms), eager on grids
-        mode = B.EngineMode.Lazy if b.m >= 8 * max(b.n, 1) else B.EngineMode.Eager
+    if args.mode == "b200":
+        # measured: lazy wins on large Kron and urand (C3 2.7 vs 4.75 ms), eager on grids (many
+        # levels) and on small graphs, where lazy's ~15 µs fixed stage-2 cost per level
+        # dominates (C1 RMAT-16: eager 0.091 vs lazy 0.218 ms per BFS)
+        mode = B.EngineMode.Lazy if (b.m >= 8 * max(b.n, 1) and b.num_vss >= (1 << 20)) else B.EngineMode.Eager
     else:
         cfg = B.EngineConfig(mode=B.engine_mode_from_string(args.mode), pull=args.pull)
         mode = B.choose_mode(b, plan, cfg)
