@@ -13,10 +13,13 @@
 //
 // Stage 2 (word sweep, :296-338) is lazy_stage2 (bfs_device.cuh): balanced, no contended
 // atomics; it emits the next queue as the ascending list SL of active slice sets (set id,
-// first queue position). The next level first expands SL into the materialised queue —
+// first queue position). A dense level first expands SL into the materialised queue —
 // every warp writes an equal contiguous share of positions, resolving sets with a
 // 32-set window in its lanes — then a grid barrier, then stage 1. A hub set with
-// thousands of VSSs is thus spread over all warps instead of one.
+// thousands of VSSs is thus spread over all warps instead of one. A sparse level
+// (T < dense_min) skips the queue and the barrier: each warp expands its own contiguous
+// share into registers and pulls it directly. The frontier words alternate between B2
+// and B3 by level parity, so the next level's can be cleared while this one is read.
 #include "bfs.cuh"
 #include "bfs_device.cuh"
 
