@@ -6,18 +6,27 @@
 A step is one BFS (init_state + every level, one fused cooperative launch) from the next
 seeded source on the resident BVSS. Default workload (BASELINE.json configs[1]):
 GAP-style Kronecker scale 24 (RMAT a/b/c = .57/.19/.19, edgefactor 16, GAP-style random
-relabel), compression-oriented reorder (auto plan -> Jaccard windows w = 2^16), auto
-engine choice. Graph generation, reordering and BVSS construction run on the GPU before
+relabel), compression-oriented reorder (auto plan -> Jaccard windows w = 2^16), engine
+policy "b200". Graph generation, reordering and BVSS construction run on the GPU before
 the timed region. Inputs (3.4 GB BVSS) exceed the 126 MB L2, so no flush is needed.
+
+Parity (default on, outside the timed region): the ORIGINAL graph is rebuilt on the host
+from the generator twins (oracle/, orc_gen_csr: generate -> relabel -> from_edges), the
+CPU reference BFS (orc_reference_bfs, R:src/graph.cpp:144-167) runs from every timed
+source in original ids, and the GPU level arrays, mapped back through the ordering
+permutation, must equal it bit for bit; the line's "parity" block reports the count.
+The cpu_baseline leg's reference-engine levels are compared with the GPU levels too.
 
 N > 1 (torchrun): every rank holds the full structure and runs its own share of the
 sources (no data-path collective, "scaling": "weak"); value = sum over ranks of each
 rank's harmonic-mean GTEPS, each rank timed on its device, the max elapsed over ranks
 reported.
 
---impl reference: the UNMODIFIED reference engine (oracle/_ref: R:src/bfs_engine.cpp
-run_eager/run_lazy, with workers = all host threads, num_warps = 32 x threads) over the
-same BVSS arrays and sources, on a bounded sample of steps.
+--impl reference: host CPU only — the product library is never loaded. The structure is
+built by the CPU oracle (generator twins, classifier, Jaccard windows / RCM restatements,
+BVSS builder; each pinned to the reference) and the UNMODIFIED reference engine
+(oracle/_ref: R:src/bfs_engine.cpp run_eager/run_lazy, workers = all host threads,
+num_warps = 32 x threads) is timed over it from the same sources, on a bounded sample.
 """
 from __future__ import annotations
 
@@ -71,29 +80,54 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons, sampled every 20 ms from before the timed region
-    (nvidia-smi needs ~0.1 s to start); summary() keeps the samples read while the timed
-    region ran (mark()/unmark() bracket it), or the nearest ones when it was shorter."""
+    """SM clocks + throttle reasons sampled in-process through NVML every few ms from a
+    background thread (no subprocess start-up lag), started before the warm-up so it is
+    sampling when the timed region begins; summary() keeps the samples taken while the
+    timed region ran (mark()/unmark() bracket it), or the nearest ones when it was
+    shorter than the sampling period."""
 
-    def __init__(self, index: int):
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
+
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
-        self.rows = []  # (host time, fields)
-        self.proc = None
+        self.period = period_s
+        self.rows = []  # (host time, [sm_mhz, sm_max_mhz, reasons bitmask])
         self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.thread = None
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = self._handle(nv)
+            self.sm_max = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: the summary says "unsampled"
+            log(f"clock sampler unavailable: {e}")
+            return self
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+        while not self.rows and self.thread.is_alive():  # the first sample precedes the timed region
+            time.sleep(self.period)
         return self
+
+    def _handle(self, nv):
+        # CUDA and NVML enumerate devices in the same (PCI) order when CUDA_VISIBLE_DEVICES is
+        # unset, as on the bench box; the process's device index is its local rank
+        return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((time.time(), [sm, self.sm_max, rs]))
+            except Exception:
+                return
+            time.sleep(self.period)
 
     def mark(self):
         self.t0 = time.time()
@@ -101,24 +135,15 @@ class ClockSampler:
     def unmark(self):
         self.t1 = time.time()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append((time.time(), parts))
-
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread:
+            self.thread.join(timeout=1)
 
     def summary(self):
-        rows = self.rows
+        rows = list(self.rows)
         if self.t0 is not None and self.t1 is not None and rows:
-            inside = [r for t, r in rows if self.t0 <= t <= self.t1 + 0.05]
+            inside = [r for t, r in rows if self.t0 <= t <= self.t1]
             if not inside:  # region shorter than the sampling period: the nearest samples
                 mid = 0.5 * (self.t0 + self.t1)
                 inside = [r for t, r in sorted(rows, key=lambda tr: abs(tr[0] - mid))[:3]]
@@ -127,16 +152,55 @@ class ClockSampler:
             rows = [r for _, r in rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({name for r in rows for name, bit in self.REASONS if int(r[2]) & bit})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": max(float(r[1]) for r in rows),
+                "reasons": reasons, "samples": len(rows), "source": "NVML in-process"}
 
 
-def prepare(config: str, ordering_override: str | None, window: int, prepass: str = "none",
-            postpass: str = "none"):
+def oracle_mod():
+    """The CPU checker (oracle/): only the parity, cpu_baseline and reference legs use it."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    return O
+
+
+def cpu_original_graph(config: str, threads: int):
+    """The config's ORIGINAL graph (before the ordering) built on the host by the oracle's
+    generator twins: the same (seed, index) -> edge functions as the device generators,
+    the same relabel, then Graph::from_edges semantics (R:src/graph.cpp:33-55)."""
+    O = oracle_mod()
+    kind, prm, _, _ = CONFIGS[config]
+    if kind == "rmat":
+        n = 1 << prm["scale"]
+        spec = ("rmat", prm["scale"], 0, prm["ef"] << prm["scale"], prm["seed"])
+    elif kind == "urand":
+        n = 1 << prm["scale"]
+        spec = ("urand", n, 0, prm["ef"] * n, prm["seed"])
+    else:
+        n = prm["rows"] * prm["cols"]
+        spec = ("grid", prm["rows"], prm["cols"], 0, 0)
+    fw = O.random_relabel_mt(n, prm["relabel"], threads) if prm.get("relabel") is not None else None
+    return O.gen_csr(*spec, forward=fw, threads=threads)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def engine_policy_lazy(n: int, m: int, num_vss: int) -> bool:
+    """bench engine policy "b200": lazy unless the graph is low-degree (arcs/n < 8: grids,
+    thousands of levels, where eager's one barrier per level wins) or small (< 2^20 VSSs,
+    where lazy's fixed stage-2 cost per level dominates)."""
+    return m >= 8 * max(n, 1) and num_vss >= (1 << 20)
+
+
+def prepare(config: str, ordering_override: str | None, window: int):
     """Generate -> (relabel) -> plan/order -> permute -> build, all on the GPU."""
     import paper_2512_21967_b200 as B
     kind, prm, ordering, desc = CONFIGS[config]
@@ -155,11 +219,8 @@ def prepare(config: str, ordering_override: str | None, window: int, prepass: st
     t0 = time.time()
     force = {"auto": None, "identity": B.OrderingStrategy.Identity, "rcm": B.OrderingStrategy.Rcm,
              "jaccard": B.OrderingStrategy.JaccardWindows, "random": B.OrderingStrategy.Random}[ordering]
-    pre = B.PrePass.DegreeSort if prepass == "degree" else B.PrePass.None_
-    plan = B.select_plan(g, 8, B.SelectDefaults(window_size=window, force=force, pre_pass=pre))
+    plan = B.select_plan(g, 8, B.SelectDefaults(window_size=window, force=force))
     perm = B.make_permutation(g, plan, 8, seed=7)
-    if postpass == "hub-blocks":
-        perm = B.api.hub_blocks(g, perm)
     t_order = time.time() - t0
     t0 = time.time()
     gp = g if perm.is_identity() else B.apply_permutation(g, perm)
@@ -172,14 +233,18 @@ def prepare(config: str, ordering_override: str | None, window: int, prepass: st
 
 
 def b_alg(n, D, P, V, L, lazy):
-    """Algorithmic bytes per BFS: 648 D + 4 P + 4 n + 4 V + k (n/8) L."""
-    return 648 * D + 4 * P + 4 * n + 4 * V + (2 if lazy else 1) * (n // 8) * L
+    """Algorithmic bytes per BFS: 648 D + 4 P + 4 n + 4 V + k (n/8) L with
+    k = 2 for lazy (the V_curr + V_next word sweep of every level) and k = 0 for eager: the
+    reference clears F_next (n/8 bytes) every level, the B200 eager engine never does (its
+    triple-buffered frontier zeroes only the bytes the previous level set)."""
+    return 648 * D + 4 * P + 4 * n + 4 * V + (2 if lazy else 0) * (n // 8) * L
 
 
-def cpu_reference_sample(prep, sources_bvss, mode_lazy, budget_s, threads, max_steps):
-    """Time the reference engine (oracle/_ref) on a bounded sample of the same workload."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+def cpu_reference_sample(prep, sources_bvss, mode_lazy, budget_s, threads, max_steps, gpu_levels=None):
+    """Time the reference engine (oracle/_ref) on a bounded sample of the same workload, over
+    the GPU-built BVSS arrays. With gpu_levels (source -> level array, permuted ids) every
+    sampled source's reference-engine levels are compared with the GPU's."""
+    O = oracle_mod()
     b = prep["b"]
     rp, v2r, rows, masks = b.arrays()
     arr = O.BvssArrays(b.n, b.m, b.num_slice_sets, b.num_vss, b.num_unpadded_slices, rp, v2r, rows, masks)
@@ -187,23 +252,124 @@ def cpu_reference_sample(prep, sources_bvss, mode_lazy, budget_s, threads, max_s
         rb = O.ref_bvss_from_arrays(arr)
         kind = "reference"
         run = lambda s: rb.run(int(s), mode_lazy, warps=32 * threads, workers=threads,
-                               want_levels=False, n=b.n, trace_cap=1 << 16)
+                               want_levels=True, n=b.n, trace_cap=1 << 16)
         cores = threads
     else:
         kind = "port"
         run = lambda s: O.run_engine(arr, int(s), mode_lazy)
         cores = 1
-    times, counters = [], []
+    times, counters, checked, mism = [], [], 0, 0
     t_start = time.time()
     for s in sources_bvss[:max_steps]:
         t0 = time.perf_counter()
         r = run(s)
         times.append(time.perf_counter() - t0)
         counters.append(r.counters)
+        if gpu_levels is not None and int(s) in gpu_levels:
+            checked += 1
+            mism += int(not np.array_equal(r.levels, gpu_levels[int(s)]))
         if time.time() - t_start > budget_s:
             break
     del arr
-    return kind, cores, times, counters
+    return kind, cores, times, counters, dict(checked=checked, mismatches=mism)
+
+
+def validate_levels(config, threads, srcs_orig, gpu_levels, fwd, edges):
+    """Parity of the timed sources against the CPU reference BFS on the host-built ORIGINAL
+    graph: GPU levels (permuted ids) mapped back through the ordering (levels_orig[v] =
+    levels_gpu[forward[v]]) must equal orc_reference_bfs's; the traversed-edge numerator
+    and the non-isolated source picks are cross-checked too."""
+    O = oracle_mod()
+    t0 = time.time()
+    g = cpu_original_graph(config, threads)
+    t_graph = time.time() - t0
+    t0 = time.time()
+    want, _ = O.reference_bfs_many(g, np.asarray(srcs_orig, np.uint32), threads)
+    t_bfs = time.time() - t0
+    mism, bad_edges = [], 0
+    for k, s in enumerate(srcs_orig):
+        got = gpu_levels[k] if fwd is None else gpu_levels[k][fwd]
+        if not np.array_equal(got, want[k]):
+            mism.append(int(s))
+        if O.traversed_edges(g, want[k]) != edges[k]:
+            bad_edges += 1
+    return dict(checked=len(srcs_orig), mismatches=len(mism), mismatched_sources=mism[:8],
+                edges_mismatches=bad_edges,
+                oracle="orc_reference_bfs (R:src/graph.cpp:144-167) from the original source ids on the "
+                       "host-built original graph (orc_gen_csr generator twins + relabel + from_edges); "
+                       "GPU levels mapped back through the ordering permutation",
+                cpu_graph_s=round(t_graph, 1), cpu_bfs_s=round(t_bfs, 1), threads=threads), g
+
+
+def run_reference(args):
+    """--impl reference: host CPU only, the product library is never loaded. Structure by the
+    pinned CPU oracle (generator twins -> classifier -> Jaccard windows / RCM -> permute ->
+    BVSS), then the UNMODIFIED reference engine (oracle/_ref, R:src/bfs_engine.cpp
+    run_eager / run_lazy) timed from the same sources as our arm's rank 0."""
+    O = oracle_mod()
+    threads = os.cpu_count() or 1
+    kind, prm, ordering, desc = CONFIGS[args.config]
+    ordering = args.order or ordering
+    t0 = time.time()
+    g = cpu_original_graph(args.config, threads)
+    t_gen = time.time() - t0
+    t0 = time.time()
+    n = g.n
+    cls = O.classify(g)
+    strategy = {"auto": "jaccard-windows" if cls["is_social_like"] else "rcm", "identity": "identity",
+                "rcm": "rcm", "jaccard": "jaccard-windows"}[ordering]
+    if strategy == "jaccard-windows":
+        fwd = O.jaccard_windows(g, args.window, 8, threads)
+    elif strategy == "rcm":
+        fwd = O.rcm(g)
+    else:
+        fwd = None
+    t_order = time.time() - t0
+    t0 = time.time()
+    gp = O.permute_csr(g, fwd, threads) if fwd is not None else g
+    arr = O.build_bvss_mt(gp, threads)
+    rb = O.ref_bvss_from_arrays(arr)
+    t_build = time.time() - t0
+    lazy = engine_policy_lazy(n, arr.m, arr.num_vss) if args.mode == "b200" else (args.mode == "lazy")
+    total = args.steps * max(args.gpus, 1) + args.warmup
+    srcs_orig = O.pick_sources(g, total, args.source_seed)
+    srcs = fwd[srcs_orig] if fwd is not None else srcs_orig
+    warm, mine = srcs[: args.warmup], srcs[args.warmup: args.warmup + args.steps]
+    run = lambda s: rb.run(int(s), lazy, warps=32 * threads, workers=threads, want_levels=True, n=n,
+                           trace_cap=1 << 16)
+    for s in warm:
+        run(s)
+    times, edges, t_start = [], [], time.time()
+    for s in mine:
+        t1 = time.perf_counter()
+        r = run(s)
+        times.append(time.perf_counter() - t1)
+        edges.append(O.traversed_edges(gp, r.levels))
+        if time.time() - t_start > 150.0:
+            break
+    # self-check of the timed engine against the CPU reference BFS (first source, untimed)
+    want = O.reference_bfs(g, int(srcs_orig[args.warmup]))[0]
+    got = run(mine[0]).levels
+    ok = bool(np.array_equal(got if fwd is None else got[fwd], want))
+    hm = len(times) / sum(t / e for t, e in zip(times, edges)) / 1e9
+    workload = dict(workload=args.config, graph=desc, n=n, arcs=int(arr.m), num_vss=int(arr.num_vss),
+                    ordering=strategy, engine="lazy" if lazy else "eager", engine_policy=args.mode,
+                    sources=len(times), source_seed=args.source_seed,
+                    prep_s=dict(generate_s=round(t_gen, 3), order_s=round(t_order, 3), build_s=round(t_build, 3)),
+                    parallelism=f"{threads} host threads")
+    cpu = dict(value=round(hm, 6), unit="GTEPS", cores=threads, kind="reference" if O.ref_available() else "port",
+               cpu_model=cpu_model(),
+               sample=f"{len(times)} of {args.steps} sources (bounded ~150 s) after {len(warm)} warm-up runs, "
+                      f"R:src/bfs_engine.cpp run_{'lazy' if lazy else 'eager'} workers={threads} "
+                      f"num_warps={32 * threads} over a BVSS built by the CPU oracle (no GPU)")
+    line = dict(metric="GTEPS (harmonic mean over sources)", value=round(hm, 6), unit="GTEPS", n_gpus=args.gpus,
+                steps=len(times), warmup=len(warm), ms_per_step=round(1e3 * sum(times) / len(times), 3),
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
+                impl="reference", config=workload, cpu_baseline=cpu,
+                e2e=dict(value=round(hm, 6), unit="GTEPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                parity=dict(checked=1, mismatches=int(not ok),
+                            oracle="reference engine levels vs orc_reference_bfs (first timed source)"))
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -220,15 +386,15 @@ def main():
     ap.add_argument("--pull", default="popc", choices=["popc", "mma"])
     ap.add_argument("--order", default=None, choices=["auto", "identity", "rcm", "jaccard", "random"])
     ap.add_argument("--window", type=int, default=1 << 16)
-    ap.add_argument("--prepass", default="none", choices=["none", "degree"])
-    ap.add_argument("--postpass", default="none", choices=["none", "hub-blocks"])
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (256/512/1024; 0 = default)")
     ap.add_argument("--grid-ctas", type=int, default=0, help="persistent grid size (0 = all co-resident CTAs)")
     ap.add_argument("--source-seed", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--validate", type=int, default=0, help="check this many sources against the CPU oracle")
+    ap.add_argument("--validate", type=int, default=-1,
+                    help="parity: check this many timed sources against the CPU reference BFS on a host-built "
+                         "original graph (-1 = all, 0 = off)")
     ap.add_argument("--partition", default="replicas", choices=["replicas", "rows"],
                     help="N>1: source-sharded replicas (default) or one BFS row-partitioned over the ranks")
     ap.add_argument("--virtual-ranks", type=int, default=0,
@@ -240,9 +406,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if rank != 0:
-            return  # the reference arm runs on rank 0 only, the other ranks exit without work
-        world = 1  # ... and without a process group (nobody else would join it)
+        if rank == 0:  # rank 0 alone runs it; the other ranks exit without work
+            run_reference(args)
+        return
 
     import torch
     import torch.distributed as dist
@@ -265,13 +431,13 @@ def main():
     stream = torch.cuda.current_stream()
     L.check(lib.blest_set_stream(C.c_void_p(stream.cuda_stream)))
 
-    prep = prepare(args.config, args.order, args.window, args.prepass, args.postpass)
+    prep = prepare(args.config, args.order, args.window)
     g, b, plan, perm = prep["g"], prep["b"], prep["plan"], prep["perm"]
     if args.mode == "b200":
         # measured: lazy wins on large Kron and urand (C3 2.7 vs 4.75 ms), eager on grids (many
         # levels) and on small graphs, where lazy's ~15 µs fixed stage-2 cost per level
         # dominates (C1 RMAT-16: eager 0.091 vs lazy 0.218 ms per BFS)
-        mode = B.EngineMode.Lazy if (b.m >= 8 * max(b.n, 1) and b.num_vss >= (1 << 20)) else B.EngineMode.Eager
+        mode = B.EngineMode.Lazy if engine_policy_lazy(b.n, b.m, b.num_vss) else B.EngineMode.Eager
     else:
         cfg = B.EngineConfig(mode=B.engine_mode_from_string(args.mode), pull=args.pull)
         mode = B.choose_mode(b, plan, cfg)
@@ -285,7 +451,7 @@ def main():
     threads = os.cpu_count() or 1
     workload = dict(workload=args.config, graph=prep["desc"], n=n, arcs=int(b.m),
                     num_vss=int(b.num_vss), ordering=plan.strategy.value, engine=mode.value, engine_policy=args.mode,
-                    pull=args.pull, prepass=args.prepass, postpass=args.postpass, sources=len(mine) * world, source_seed=args.source_seed,
+                    pull=args.pull, sources=len(mine) * world, source_seed=args.source_seed,
                     l2=("inputs larger than L2 (BVSS %.2f GB > 126 MB), no flush" % (b.num_vss * 644 / 1e9)
                         if b.num_vss * 644 >= 2 * 126e6 else
                         "BVSS %.1f MB fits in L2: 512 MB L2 flush before every timed BFS" % (b.num_vss * 644 / 1e6)),
@@ -295,42 +461,36 @@ def main():
         run_partitioned(args, prep, B, L, lib, srcs_orig, perm, world, rank, local, workload, stream)
         return
 
-    if args.impl == "reference":
-        t0 = time.time()
-        kind, cores, times, ctrs = cpu_reference_sample(prep, mine, lazy, budget_s=150.0, threads=threads,
-                                                        max_steps=args.steps)
-        # traversed edges per source (bookkeeping for the metric, outside the timed region)
-        ev = [c["E"] for c in census_of(lib, L, b, prep, mine[: len(times)], lazy, args.pull)]
-        hm = len(times) / sum(t / e for t, e in zip(times, ev)) / 1e9
-        line = dict(metric="GTEPS (harmonic mean over sources)", value=round(hm, 6), unit="GTEPS",
-                    n_gpus=1, steps=len(times), warmup=0, ms_per_step=round(1e3 * sum(times) / len(times), 3),
-                    higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
-                    impl="reference", config=workload,
-                    cpu_baseline=dict(value=round(hm, 6), unit="GTEPS", cores=cores, kind=kind,
-                                      sample=f"{len(times)} of {args.steps} sources (bounded ~150 s), "
-                                             f"R:src/bfs_engine.cpp run_{'lazy' if lazy else 'eager'} "
-                                             f"workers={cores} num_warps={32 * cores}"),
-                    e2e=dict(value=round(hm, 6), unit="GTEPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
-        print(json.dumps(line), flush=True)
-        return
-
     ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
                            L.PULL_MMA if args.pull == "mma" else L.PULL_POPC, 0, 0, args.grid_ctas, args.threads)
     ctr = L.CountersT()
-    # ---- census (untimed): deterministic counters + traversed edges per source ----
-    census = census_of(lib, L, b, prep, mine, lazy, args.pull, args.threads, args.grid_ctas)
-    if args.validate:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import oracle as O
-        off, tgt = prep["gp"].csr()
-        csr = O.Csr(n, off, tgt)
-        chk = mine[: args.validate]
-        want, _ = O.reference_bfs_many(csr, chk)
-        lv = np.zeros(n, np.uint32)
-        for k, s in enumerate(chk):
-            L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), lv.ctypes.data, C.byref(ctr), None, 0))
-            assert np.array_equal(lv, want[k]), f"levels mismatch for source {int(s)}"
-        log(f"validated {len(chk)} sources bit-exact against the CPU oracle")
+    # ---- engine preparation (lazy: the hot-row view), timed and sized apart from the BFS ----
+    t0 = time.time()
+    ebytes = C.c_uint64()
+    L.check(lib.blest_bfs_prepare(b.handle, C.byref(ecfg), C.byref(ebytes)))
+    prep["times"]["engine_prepare_s"] = round(time.time() - t0, 3)
+    workload["engine_device_bytes"] = int(ebytes.value)
+    workload["bvss_device_bytes"] = int(4 * (b.num_slice_sets + 1) + 4 * b.num_vss + 4 * 128 * b.num_vss
+                                        + 4 * 32 * b.num_vss)
+    # ---- census (untimed): deterministic counters + traversed edges (+ levels) per source ----
+    nval = len(mine) if args.validate < 0 else min(args.validate, len(mine))
+    if world > 1 and rank != 0:
+        nval = 0  # replicas run the same code path: rank 0 validates its share
+    keep = {int(s) for s in mine[:max(nval, 8)]}
+    census = census_of(lib, L, b, prep, mine, lazy, args.pull, args.threads, args.grid_ctas, keep_levels=keep)
+    parity = None
+    if nval:
+        fm = None if perm.is_identity() else perm.forward_map()
+        srcs_mine_orig = srcs_orig[args.warmup + rank * args.steps: args.warmup + rank * args.steps + nval]
+        parity, gcpu = validate_levels(args.config, threads, srcs_mine_orig,
+                                       [census[k]["levels"] for k in range(nval)], fm,
+                                       [census[k]["E"] for k in range(nval)])
+        O = oracle_mod()
+        parity["source_picks_match"] = bool(np.array_equal(O.pick_sources(gcpu, total_sources, args.source_seed),
+                                                           srcs_orig))
+        del gcpu
+        log(f"parity: {parity['checked']} sources, {parity['mismatches']} mismatches "
+            f"(cpu graph {parity['cpu_graph_s']} s, cpu bfs {parity['cpu_bfs_s']} s)")
     # ---- warmup (the clock sampler starts here so it is running in the timed region) ----
     clk = ClockSampler(local).start()
     for s in warm:
@@ -406,11 +566,28 @@ def main():
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        kind, cores, ctimes, _ = cpu_reference_sample(prep, mine, lazy, args.cpu_budget, threads, max_steps=8)
+        glv = {int(mine[k]): census[k]["levels"] for k in range(len(mine)) if census[k].get("levels") is not None}
+        kind, cores, ctimes, _, echeck = cpu_reference_sample(prep, mine, lazy, args.cpu_budget, threads,
+                                                              max_steps=8, gpu_levels=glv)
         chm = len(ctimes) / sum(tc / e for tc, e in zip(ctimes, E[: len(ctimes)])) / 1e9
-        cpu = dict(value=round(chm, 6), unit="GTEPS", cores=cores, kind=kind,
+        cpu = dict(value=round(chm, 6), unit="GTEPS", cores=cores, kind=kind, cpu_model=cpu_model(),
                    sample=f"first {len(ctimes)} of the {len(mine)} timed sources (~{args.cpu_budget:.0f} s budget), "
-                          f"run_{'lazy' if lazy else 'eager'} over the same BVSS arrays")
+                          f"run_{'lazy' if lazy else 'eager'} over the same BVSS arrays",
+                   engine_levels_vs_gpu=echeck)
+        # reference_bfs on one core (R:src/graph.cpp:144-167, the oracle's restatement), one source
+        O = oracle_mod()
+        g1 = O.Csr(n, *prep["gp"].csr())
+        t1 = time.perf_counter()
+        lv1 = O.reference_bfs(g1, int(mine[0]))[0]
+        t1 = time.perf_counter() - t1
+        cpu["reference_bfs_1core"] = dict(value=round(census[0]["E"] / t1 / 1e9, 6), unit="GTEPS", cores=1,
+                                          kind="port", seconds=round(t1, 3),
+                                          levels_match_gpu=bool(census[0].get("levels") is None or
+                                                                np.array_equal(lv1, census[0]["levels"])),
+                                          sample="first timed source, orc_reference_bfs (FIFO queue BFS)")
+        if parity is not None:
+            parity["engine_levels_vs_gpu"] = echeck
+        del g1
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
@@ -429,7 +606,7 @@ def main():
                           peak_source=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
                           algorithmic_bytes_per_bfs=int(np.mean(balg)),
                           formula="648 D + 4 P + 4 n + 4 V + k (n/8) L (SURVEY 8(d))"),
-            cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
+            cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches), parity=parity,
             clocks=clk.summary(),
             detail=dict(grid=[g_ctas.value, g_thr.value], hm_gteps_rank0=round(hm, 4), mean_ms=round(1e3 * float(t.mean()), 4),
                         min_ms=round(1e3 * float(t.min()), 4), max_ms=round(1e3 * float(t.max()), 4),
@@ -508,19 +685,23 @@ def run_partitioned(args, prep, B, L, lib, srcs_orig, perm, world, rank, local, 
                               config=workload, detail=dict(mean_traversed_edges=int(E.mean())))), flush=True)
 
 
-def census_of(lib, L, b, prep, sources, lazy, pull, threads=0, grid_ctas=0):
+def census_of(lib, L, b, prep, sources, lazy, pull, threads=0, grid_ctas=0, keep_levels=()):
     """Per source: VSS dequeues D, pushes P, visited V, level iterations L and traversed
-    undirected edges E (on the permuted graph, whose ids the level array uses)."""
+    undirected edges E (on the permuted graph, whose ids the level array uses); the level
+    array itself (host copy, permuted ids) for the sources in keep_levels."""
     ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
                            L.PULL_MMA if pull == "mma" else L.PULL_POPC, 0, 0, grid_ctas, threads)
     ctr = L.CountersT()
     lv_ptr = C.c_void_p()
     out = []
     for s in sources:
-        L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), None, C.byref(ctr), None, 0))
+        lv = np.empty(b.n, np.uint32) if int(s) in keep_levels else None
+        L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), lv.ctypes.data if lv is not None else None,
+                              C.byref(ctr), None, 0))
         L.check(lib.blest_bfs_levels_device(b.handle, C.byref(lv_ptr)))
         e = prep["gp"].traversed_edges(lv_ptr.value)
-        out.append(dict(D=ctr.vss_dequeues, P=ctr.queue_pushes, V=ctr.visited_count, L=ctr.trace_len, E=e))
+        out.append(dict(D=ctr.vss_dequeues, P=ctr.queue_pushes, V=ctr.visited_count, L=ctr.trace_len, E=e,
+                        levels=lv))
     return out
 
 

@@ -95,13 +95,6 @@ int blest_order_rcm(blest_graph g, uint32_t* forward);
 /* jaccard_with_windows(g, sigma, w, nullptr) (R:include/blest/ordering.hpp:52-53,
  * R:src/ordering.cpp:139-166) — one CTA per window on the GPU. */
 int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint32_t* forward);
-/* Hub-first pre-pass (new; composable like R:include/blest/ordering.hpp PrePass):
- * forward[u] = rank of (out-degree descending, id ascending). */
-int blest_order_degree(blest_graph g, uint32_t* forward, int host);
-/* Hub-block post-pass (new): after `base_forward` (host, may be NULL = identity), order the
- * 8-id slice-set blocks by descending degree sum, keeping each block intact (slice sets,
- * compression and VSS dequeues unchanged). Writes the composed forward map (host). */
-int blest_order_hub_blocks(blest_graph g, const uint32_t* base_forward, uint32_t* forward);
 /* random_order(n, seed) (R:include/blest/ordering.hpp:58, R:src/ordering.cpp:268-275). */
 int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward);
 /* Harness relabel: forward[i] = rank of (splitmix64(seed, i), i); host or device output. */
@@ -185,10 +178,22 @@ int blest_bfs_finish(blest_bvss b, uint32_t* levels_out, blest_counters* counter
 /* Per-level device timestamps of the last finished run (%globaltimer ns, 3 per level:
  * level start, lazy stage-1 end, level end); *rows = levels recorded. */
 int blest_bfs_phase_times(blest_bvss b, uint64_t* out, uint32_t cap, uint32_t* rows);
+/* Build what runs of `cfg` need before the first BFS (lazy: the hot-row view of the visited
+ * bitmaps) and report the engine's device bytes (workspace + view); optional — the first
+ * BFS builds it otherwise. No reference counterpart (device workspace). */
+int blest_bfs_prepare(blest_bvss b, const blest_engine_config* cfg, uint64_t* engine_bytes);
 /* Device pointer to the level array of the last run on b (n entries). */
 int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
 /* Launch geometry of the last run (CTAs, threads per CTA). */
 int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads);
+
+/* ---- tile known-answer entry (R:src/tc_emu.cpp:9-45) -------------------------------- */
+/* One warp per tile runs the engines' b1 pull (2 x mma.sync.m8n8k128.b1.and.popc with
+ * BLEST's fragB broadcast of alpha, build_fragB / pack_fragA_round) on the device:
+ * masks[32*t + lane] and alpha[t] in, counts[128*t + 64*round + 8*i + j] = FragC(i, j) of
+ * round 0/1 out (host arrays) — tc::mma_m8n8k128(pack_fragA_round(masks, round),
+ * build_fragB(alpha)). For the reference's tile KATs (R:tests/tc_emu_test.cpp:186-241). */
+int blest_tile_pull(const uint32_t* masks, const uint8_t* alpha, uint32_t count, uint32_t* counts);
 
 /* ---- row-partitioned multi-GPU mode (no reference counterpart) ---------- */
 /* BVSS of A[rows [row_lo, row_hi), all columns] (row_lo 32-aligned, row_hi 32-aligned or n):

@@ -73,6 +73,30 @@ int64_t orc_run_engine(uint32_t n, const uint32_t* real_ptrs, uint64_t num_vss, 
                        uint32_t num_warps, uint32_t max_levels, uint32_t* levels,
                        uint64_t* trace, uint64_t trace_cap);
 
+/* ---- full scale (blest_oracle_scale.c): multi-threaded, same results ---- */
+void orc_free(void* p);
+/* Generator twin (kind 0 RMAT(scale=a, k edges, seed, thresholds t0..t2), 1 urand(n=a, k
+ * edges, seed), 2 grid(rows=a, cols=b)) -> optional relabel (forward map, may be NULL) ->
+ * Graph::from_edges(undirected). *off / *tgt are malloc'd (orc_free). Returns m. */
+uint64_t orc_gen_csr(int kind, uint32_t a, uint32_t b, uint64_t k, uint64_t seed, uint32_t t0,
+                     uint32_t t1, uint32_t t2, const uint32_t* forward, int threads,
+                     uint64_t** off, uint32_t** tgt);
+void orc_random_relabel_mt(uint32_t n, uint64_t seed, int threads, uint32_t* forward);
+uint64_t orc_permute_csr(uint32_t n, const uint64_t* off, const uint32_t* tgt, const uint32_t* forward,
+                         int threads, uint64_t* off_out, uint32_t* tgt_out);
+uint64_t orc_transpose_csr(uint32_t n, const uint64_t* off, const uint32_t* tgt, uint64_t* ioff,
+                           uint32_t* isrc);
+uint64_t orc_symmetrise_csr(uint32_t n, const uint64_t* off, const uint32_t* tgt, const uint64_t* ioff,
+                            const uint32_t* isrc, uint64_t* aoff, uint32_t* atgt);
+int orc_jaccard_windows(uint32_t n, const uint64_t* off, const uint32_t* tgt, const uint64_t* ioff,
+                        const uint32_t* isrc, uint32_t sigma, uint32_t w, int threads, uint32_t* forward);
+void orc_rcm(uint32_t n, const uint64_t* aoff, const uint32_t* atgt, uint32_t* forward);
+uint64_t orc_bvss_count_mt(uint32_t n, const uint64_t* off, const uint32_t* tgt, int threads,
+                           uint32_t* real_ptrs, uint64_t* num_unpadded);
+void orc_bvss_fill_mt(uint32_t n, const uint64_t* off, const uint32_t* tgt, const uint32_t* real_ptrs,
+                      int threads, uint32_t* v2r, uint32_t* row_ids, uint32_t* masks);
+uint64_t orc_traversed_edges(uint32_t n, const uint64_t* off, const uint32_t* levels);
+
 /* Tile semantics of one pull round (R:src/tc_emu.cpp:9-45): c64 = FragC counts. */
 void orc_tile_pull(const uint32_t* mask_words, uint8_t alpha, unsigned round, uint32_t* c64);
 

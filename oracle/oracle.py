@@ -78,6 +78,27 @@ def orc():
                                      C.c_uint32, C.c_int, C.c_uint32, C.c_uint32, _u32p, _u64p,
                                      C.c_uint64]
         L.orc_tile_pull.argtypes = [_u32p, C.c_uint8, C.c_uint, _u32p]
+        vp = C.c_void_p
+        L.orc_free.argtypes = [vp]
+        L.orc_gen_csr.restype = C.c_uint64
+        L.orc_gen_csr.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32,
+                                  C.c_uint32, C.c_uint32, vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
+        L.orc_random_relabel_mt.argtypes = [C.c_uint32, C.c_uint64, C.c_int, _u32p]
+        L.orc_permute_csr.restype = C.c_uint64
+        L.orc_permute_csr.argtypes = [C.c_uint32, _u64p, _u32p, _u32p, C.c_int, _u64p, _u32p]
+        L.orc_transpose_csr.restype = C.c_uint64
+        L.orc_transpose_csr.argtypes = [C.c_uint32, _u64p, _u32p, _u64p, _u32p]
+        L.orc_symmetrise_csr.restype = C.c_uint64
+        L.orc_symmetrise_csr.argtypes = [C.c_uint32, _u64p, _u32p, _u64p, _u32p, _u64p, vp]
+        L.orc_jaccard_windows.restype = C.c_int
+        L.orc_jaccard_windows.argtypes = [C.c_uint32, _u64p, _u32p, _u64p, _u32p, C.c_uint32,
+                                          C.c_uint32, C.c_int, _u32p]
+        L.orc_rcm.argtypes = [C.c_uint32, _u64p, _u32p, _u32p]
+        L.orc_bvss_count_mt.restype = C.c_uint64
+        L.orc_bvss_count_mt.argtypes = [C.c_uint32, _u64p, _u32p, C.c_int, _u32p, C.POINTER(C.c_uint64)]
+        L.orc_bvss_fill_mt.argtypes = [C.c_uint32, _u64p, _u32p, _u32p, C.c_int, _u32p, _u32p, _u32p]
+        L.orc_traversed_edges.restype = C.c_uint64
+        L.orc_traversed_edges.argtypes = [C.c_uint32, _u64p, _u32p]
         _orc = L
     return _orc
 
@@ -554,3 +575,184 @@ def pick_sources(g: Csr, count: int, seed: int) -> np.ndarray:
         if deg[x] > 0:
             out.append(int(x))
     return np.array(out, np.uint32)
+
+
+# ----------------------------------------------------------------------------------
+# Full scale (blest_oracle_scale.c): multi-threaded builders and orderings, same results.
+# ----------------------------------------------------------------------------------
+def _threads(threads):
+    return int(threads or os.cpu_count() or 1)
+
+
+class _COwned:
+    """Keeps a malloc'd C buffer alive for the numpy view built on it."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        if self.ptr and _orc is not None:
+            _orc.orc_free(self.ptr)
+            self.ptr = None
+
+
+def _adopt(ptr, count: int, ctype, dtype) -> np.ndarray:
+    if count == 0:
+        orc().orc_free(ptr)
+        return np.zeros(0, dtype)
+    arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(count,)).view(dtype)
+    return _OwnedArray(arr, _COwned(ptr))  # views of it keep it (and the C buffer) alive
+
+
+class _OwnedArray(np.ndarray):
+    def __new__(cls, a, holder):
+        obj = np.asarray(a).view(cls)
+        obj._holder = holder
+        return obj
+
+    def __array_finalize__(self, obj):
+        if obj is not None:
+            self._holder = getattr(obj, "_holder", None)
+
+
+GEN_CSR_KINDS = {"rmat": 0, "urand": 1, "grid": 2}
+
+
+def gen_csr(kind: str, a: int, b: int = 0, k: int = 0, seed: int = 0, forward=None, abc=RMAT_ABC,
+            threads: int | None = None) -> Csr:
+    """Generator twin -> optional relabel (forward map) -> Graph::from_edges(undirected), built
+    without the mirrored arc list: kind rmat (a = scale, k edges), urand (a = n, k edges),
+    grid (a = rows, b = cols). Equal to from_edges(n, *gen_*(...)) permuted by `forward`."""
+    n = (1 << a) if kind == "rmat" else (a if kind == "urand" else a * b)
+    offp, tgtp = C.c_void_p(), C.c_void_p()
+    fw = None if forward is None else np.ascontiguousarray(forward, np.uint32)
+    m = orc().orc_gen_csr(GEN_CSR_KINDS[kind], a, b, k, seed, abc[0], abc[1], abc[2],
+                          fw.ctypes.data if fw is not None else None, _threads(threads),
+                          C.byref(offp), C.byref(tgtp))
+    off = _adopt(offp.value, n + 1, C.c_uint64, np.uint64)
+    tgt = _adopt(tgtp.value, m, C.c_uint32, np.uint32)
+    return Csr(n, off, tgt, False)
+
+
+def random_relabel_mt(n: int, seed: int, threads: int | None = None) -> np.ndarray:
+    f = np.zeros(n, np.uint32)
+    orc().orc_random_relabel_mt(n, seed, _threads(threads), f)
+    return f
+
+
+def permute_csr(g: Csr, forward, threads: int | None = None) -> Csr:
+    """apply_permutation (R:src/graph.cpp:126-134), multi-threaded."""
+    off = np.zeros(g.n + 1, np.uint64)
+    tgt = np.zeros(max(g.m, 1), np.uint32)
+    orc().orc_permute_csr(g.n, g.offsets, _nz(g.targets), np.ascontiguousarray(forward, np.uint32),
+                          _threads(threads), off, tgt)
+    return Csr(g.n, off, tgt[: g.m], g.directed)
+
+
+def transpose_csr(g: Csr) -> Csr:
+    off = np.zeros(g.n + 1, np.uint64)
+    src = np.zeros(max(g.m, 1), np.uint32)
+    orc().orc_transpose_csr(g.n, g.offsets, _nz(g.targets), off, src)
+    return Csr(g.n, off, src[: g.m], g.directed)
+
+
+def in_view(g: Csr) -> Csr:
+    """The in-view: the graph itself when undirected (its arc set is symmetric)."""
+    return g if not g.directed else transpose_csr(g)
+
+
+def jaccard_windows(g: Csr, w: int, sigma: int = 8, threads: int | None = None) -> np.ndarray:
+    """jaccard_with_windows (R:src/ordering.cpp:139-166), windows over host threads."""
+    gi = in_view(g)
+    f = np.zeros(max(g.n, 1), np.uint32)
+    rc = orc().orc_jaccard_windows(g.n, g.offsets, _nz(g.targets), gi.offsets, _nz(gi.targets), sigma, w,
+                                   _threads(threads), f)
+    if rc != 0:
+        raise ValueError("window size must be a positive multiple of sigma (sigma <= 8)")
+    return f[: g.n]
+
+
+def symmetrised(g: Csr) -> Csr:
+    """symmetrised_adjacency (R:src/ordering.cpp:171-182) as a CSR."""
+    if not g.directed:
+        return g
+    gi = transpose_csr(g)
+    off = np.zeros(g.n + 1, np.uint64)
+    m = orc().orc_symmetrise_csr(g.n, g.offsets, _nz(g.targets), gi.offsets, _nz(gi.targets), off, None)
+    tgt = np.zeros(max(m, 1), np.uint32)
+    orc().orc_symmetrise_csr(g.n, g.offsets, _nz(g.targets), gi.offsets, _nz(gi.targets), off, tgt.ctypes.data)
+    return Csr(g.n, off, tgt[:m], False)
+
+
+def rcm(g: Csr) -> np.ndarray:
+    """rcm (R:src/ordering.cpp:246-266): forward map."""
+    a = symmetrised(g)
+    f = np.zeros(max(g.n, 1), np.uint32)
+    orc().orc_rcm(g.n, a.offsets, _nz(a.targets), f)
+    return f[: g.n]
+
+
+def build_bvss_mt(g: Csr, threads: int | None = None) -> BvssArrays:
+    """build_bvss (R:src/bvss.cpp:19-101) with slice sets over host threads."""
+    t = _threads(threads)
+    sets = (g.n + 7) // 8
+    rp = np.zeros(sets + 1, np.uint32)
+    unp = C.c_uint64()
+    nv = orc().orc_bvss_count_mt(g.n, g.offsets, _nz(g.targets), t, rp, C.byref(unp))
+    v2r = np.empty(max(nv, 1), np.uint32)
+    rows = np.empty(max(nv * 128, 1), np.uint32)
+    masks = np.empty(max(nv * 32, 1), np.uint32)
+    orc().orc_bvss_fill_mt(g.n, g.offsets, _nz(g.targets), rp, t, v2r, rows, masks)
+    return BvssArrays(g.n, g.m, sets, int(nv), unp.value, rp, v2r[:nv], rows[: nv * 128], masks[: nv * 32])
+
+
+def traversed_edges(g: Csr, levels: np.ndarray) -> int:
+    """1/2 * sum of the reached vertices' out-degrees."""
+    return int(orc().orc_traversed_edges(g.n, g.offsets, np.ascontiguousarray(levels, np.uint32)))
+
+
+def classify(g: Csr) -> dict:
+    """classify_social_like(g, DegreeSide::Out) (R:src/ordering.cpp:346-387) with its log-log
+    fit (fit_log_log :315-342): same operation order, so the doubles are bit-identical."""
+    import math
+    n = g.n
+    deg = np.diff(g.offsets.astype(np.int64))
+    total = int(deg.sum())
+    rep = dict(top1_share=0.0, top10_share=0.0, power_law_slope=0.0, power_law_fit_r2=0.0,
+               is_social_like=False)
+    if n == 0 or total == 0:
+        return rep
+    srt = np.sort(deg)[::-1]
+    pref = np.cumsum(srt)
+
+    def share(percent):
+        count = int(math.floor(n * percent / 100.0 + 1e-9))
+        count = min(max(count, 1), n)
+        return float(int(pref[count - 1])) / float(total)
+
+    rep["top1_share"] = share(1.0)
+    rep["top10_share"] = share(10.0)
+    heavy = rep["top1_share"] > 0.05 and rep["top10_share"] > 0.40
+    values, counts = np.unique(deg, return_counts=True)  # std::map order: ascending degree
+    pts = [(math.log2(float(d)), math.log2(float(f))) for d, f in zip(values.tolist(), counts.tolist())
+           if d >= 2 and f >= 1]
+    slope = r2 = 0.0
+    if len(pts) >= 3:
+        sx = sy = 0.0
+        for x, y in pts:
+            sx += x
+            sy += y
+        mx, my = sx / len(pts), sy / len(pts)
+        sxx = sxy = syy = 0.0
+        for x, y in pts:
+            sxx += (x - mx) * (x - mx)
+            sxy += (x - mx) * (y - my)
+            syy += (y - my) * (y - my)
+        if sxx != 0:
+            slope = sxy / sxx
+            ss_res = syy - slope * sxy
+            r2 = (1.0 if abs(ss_res) < 1e-12 else 0.0) if syy == 0 else min(max(1.0 - ss_res / syy, 0.0), 1.0)
+    rep["power_law_slope"], rep["power_law_fit_r2"] = slope, r2
+    power = len(pts) >= 3 and -3.5 <= slope <= -1.5 and r2 >= 0.8
+    rep["is_social_like"] = bool(heavy or power)
+    return rep

@@ -100,8 +100,6 @@ SIGNATURES = {
     "blest_order_rcm": (i32, [vp, vp]),
     "blest_order_jaccard_windows": (i32, [vp, u32, u32, vp]),
     "blest_order_random": (i32, [u32, u64, vp]),
-    "blest_order_degree": (i32, [vp, vp, i32]),
-    "blest_order_hub_blocks": (i32, [vp, vp, vp]),
     "blest_relabel_permutation": (i32, [u32, u64, vp, i32]),
     "blest_pick_sources": (i32, [vp, u32, u64, i32, vp]),
     "blest_bvss_build": (i32, [vp, P(vp)]),
@@ -115,6 +113,8 @@ SIGNATURES = {
     "blest_bfs_launch": (i32, [vp, u32, P(EngineConfigT)]),
     "blest_bfs_finish": (i32, [vp, vp, P(CountersT), vp, u32]),
     "blest_bfs_batch": (i32, [vp, vp, u32, P(EngineConfigT), vp, vp]),
+    "blest_bfs_prepare": (i32, [vp, vp, P(u64)]),
+    "blest_tile_pull": (i32, [vp, vp, u32, vp]),
     "blest_bfs_levels_device": (i32, [vp, P(vp)]),
     "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),

@@ -227,7 +227,6 @@ class OrderingStrategy(enum.Enum):
 class PrePass(enum.Enum):
     None_ = "none"
     BfsLocality = "bfs-locality"
-    DegreeSort = "degree"  # B200 addition: hub-first ids (shared-memory visited cache)
 
 
 def ordering_strategy_from_string(s: str) -> OrderingStrategy:
@@ -322,25 +321,7 @@ def make_permutation(g: Graph, plan: OrderingPlan, sigma: int = 8, seed: int = 0
         return rcm(g)
     if plan.pre_pass == PrePass.BfsLocality:
         raise NotImplementedError("bfs-locality pre-pass is out of scope (SURVEY §2)")
-    if plan.pre_pass == PrePass.DegreeSort:
-        return jaccard_with_windows(g, sigma, plan.window_size, degree_order(g))
     return jaccard_with_windows(g, sigma, plan.window_size)
-
-
-def hub_blocks(g: Graph, base: Permutation | None = None) -> Permutation:
-    """Hub-block post-pass (B200 addition): 8-id slice-set blocks sorted by descending
-    degree sum after `base`; slice sets, compression and dequeues are unchanged."""
-    f = np.zeros(max(g.num_vertices(), 1), np.uint32)
-    bf = base.forward_map() if base is not None else None
-    L.check(L.lib().blest_order_hub_blocks(g.handle, _ptr(bf) if bf is not None else None, _ptr(f)))
-    return Permutation(f[: g.num_vertices()])
-
-
-def degree_order(g: Graph) -> Permutation:
-    """Hub-first pre-pass: rank by (out-degree descending, id ascending), on the GPU."""
-    f = np.zeros(max(g.num_vertices(), 1), np.uint32)
-    L.check(L.lib().blest_order_degree(g.handle, _ptr(f), 1))
-    return Permutation(f[: g.num_vertices()])
 
 
 # ------------------------------------------------------------------------------------
@@ -590,6 +571,13 @@ def run_batch(b: Bvss, srcs, mode: EngineMode, cfg: EngineConfig | None = None, 
     srcs = np.ascontiguousarray(srcs, np.uint32)
     k = len(srcs)
     lv = out if out is not None else np.zeros((k, max(b.n, 1)), np.uint32)
+    if out is not None:  # the library writes k*n 32-bit words through the pointer
+        dt = getattr(out, "dtype", None)
+        nbytes = out.element_size() if hasattr(out, "element_size") else getattr(dt, "itemsize", 0)
+        contig = out.is_contiguous() if hasattr(out, "is_contiguous") else out.flags["C_CONTIGUOUS"]
+        numel = out.numel() if hasattr(out, "numel") else out.size
+        if nbytes != 4 or not contig or numel < k * b.n:
+            raise ValueError("out must be a contiguous 32-bit buffer with at least k*n elements")
     ctr = (L.CountersT * max(k, 1))()
     cs = _cfg_struct(cfg, mode)
     ptr = lv.data_ptr() if hasattr(lv, "data_ptr") else lv.ctypes.data
@@ -634,9 +622,9 @@ def run_auto_prebuilt(b: Bvss, plan: OrderingPlan, src: int, cfg: AutoConfig | N
     mode = choose_mode(b, plan, cfg.engine)
     perm = b.producing_permutation
     mapped = perm is not None and not perm.is_identity()
-    run_src = perm.forward(src) if mapped else src
-    if mapped and src >= b.n:
+    if not 0 <= int(src) < b.n:  # before any permutation lookup (R:src/bfs_engine.cpp:31)
         raise ValueError("bfs source out of range")
+    run_src = perm.forward(src) if mapped else src
     res, cnt = _run(b, run_src, cfg.engine, mode)
     if mapped:
         res = BfsResult(source=src, levels=res.levels[perm.forward_map()],
@@ -667,3 +655,15 @@ def device_info():
     sms, ma, mi = C.c_int(), C.c_int(), C.c_int()
     L.check(L.lib().blest_device_info(name, 128, C.byref(sms), C.byref(ma), C.byref(mi)))
     return dict(name=name.value.decode(), sm_count=sms.value, cc=f"{ma.value}.{mi.value}")
+
+
+def tile_pull(masks, alpha) -> np.ndarray:
+    """The engines' b1 tile on the device (blest_tile_pull): masks [T, 32] u32, alpha [T] u8
+    -> FragC counts [T, 2 rounds, 64] (tc::mma_m8n8k128 semantics, R:src/tc_emu.cpp:9-45)."""
+    m = np.ascontiguousarray(masks, np.uint32).reshape(-1, 32)
+    a = np.ascontiguousarray(alpha, np.uint8).reshape(-1)
+    if len(a) != len(m):
+        raise ValueError("one alpha per tile")
+    out = np.zeros((max(len(m), 1), 2, 64), np.uint32)
+    L.check(L.lib().blest_tile_pull(_ptr(m) if len(m) else None, _ptr(a) if len(a) else None, len(m), _ptr(out)))
+    return out[: len(m)]

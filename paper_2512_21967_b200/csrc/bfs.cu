@@ -104,6 +104,27 @@ BfsEngine::~BfsEngine() {
     if (pinned_) cudaFreeHost(pinned_);
 }
 
+void BfsEngine::ensure_sigma() {
+    if (sigma_built_) return;
+    const char* hot = getenv("BLEST_HOT");
+    sigma_view_build(b_, sigma_, hot ? (uint32_t)atoll(hot) : 0u);
+    const uint64_t stride = sigma_.hot_words + wstride_;  // both multiples of 4 words
+    vext_.alloc(2 * stride);
+    sigma_built_ = true;
+}
+
+uint64_t BfsEngine::prepare(const EngineOptions& opt) {
+    const char* sig_env = getenv("BLEST_SIGMA");
+    if (opt.mode == Mode::Lazy && opt.sigma && !(sig_env && atoi(sig_env) == 0)) ensure_sigma();
+    CK(cudaStreamSynchronize(stream()));
+    uint64_t bytes = levels_.count * 4 + levels2_.count * 4 + bits_.count * 4 + q_.count * 8 + ctl_.count * 8 +
+                     agg_.count * 8 + aggS_.count * 8 + sl_.count * 8 + bar_.count * 4 + trace_.count * 8 +
+                     tstamp_.count * 8;
+    if (sigma_built_)
+        bytes += sigma_.rows.count * 4 + sigma_.sig.count * 4 + sigma_.inv.count * 4 + vext_.count * 4;
+    return bytes;
+}
+
 void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (src >= b_.n) throw InvalidArgument("bfs source out of range");
     const char* var_env = getenv("BLEST_LAZY_VARIANT");
@@ -161,13 +182,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
     if (sigma) {
-        if (!sigma_built_) {
-            const char* hot = getenv("BLEST_HOT");
-            sigma_view_build(b_, sigma_, hot ? (uint32_t)atoll(hot) : 0u);
-            const uint64_t stride = sigma_.hot_words + wstride_;  // both multiples of 4 words
-            vext_.alloc(2 * stride);
-            sigma_built_ = true;
-        }
+        ensure_sigma();
         const uint64_t stride = sigma_.hot_words + wstride_;
         p.B0 = vext_.p;  // V_curr / V_next = [hot prefix | row words]
         p.B1 = vext_.p + stride;
@@ -179,11 +194,15 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
     if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);
+    p.tail_div = 8;  // dense lazy levels hand out their last eighth dynamically
+    if (const char* t = getenv("BLEST_TAIL_DIV")) p.tail_div = (uint32_t)atoi(t);
+    if (const char* rc = getenv("BLEST_LAZY_RECHECK")) p.lazy_recheck = (uint32_t)atoi(rc);
     cudaStream_t st = stream();
     CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
     void* args[] = {&p};
     CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, dyn, st));
     g_launches.fetch_add(1);
+    last_levels_ = p.L;
     last_ctas_ = ctas;
     last_threads_ = threads;
     last_src_ = src;
@@ -267,7 +286,7 @@ BfsOutcome BfsEngine::finish(uint32_t* levels_host) {
     cudaStream_t st = stream();
     CK(cudaMemcpyAsync(pinned_, ctl_.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (levels_host && b_.n)
-        CK(cudaMemcpyAsync(levels_host, levels_.p, (size_t)b_.n * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(levels_host, levels_device(), (size_t)b_.n * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     BfsOutcome out;
     out.iterations = (uint32_t)pinned_[4];

@@ -14,6 +14,9 @@ namespace blestgpu {
 enum class Mode : int { Eager = 0, Lazy = 1 };
 enum class Pull : int { Popc = 0, Mma = 1 };  // CUDA-core popcount vs b1 mma.sync tile
 
+// Tile known-answer entry (tile.cu): `count` tiles, host arrays (blest_tile_pull).
+void tile_pull_device(const uint32_t* masks, const uint8_t* alpha, uint32_t count, uint32_t* counts);
+
 struct EngineOptions {
     Mode mode = Mode::Eager;
     Pull pull = Pull::Popc;
@@ -50,6 +53,10 @@ public:
     BfsEngine(const BfsEngine&) = delete;
     BfsEngine& operator=(const BfsEngine&) = delete;
 
+    // Build what launches of `opt` need up front (lazy: the hot-row view) and return the
+    // engine's device bytes (workspace + view), so a caller can time and size it apart
+    // from the BFS itself.
+    uint64_t prepare(const EngineOptions& opt);
     // Enqueue init + the fused level loop on stream() (no host sync). Throws on bad args.
     void launch(uint32_t src, const EngineOptions& opt);
     // Wait for the last launch, read back trace/counters, check status (throws
@@ -61,7 +68,8 @@ public:
     // per-source summary. Returns per-source outcomes without per-level rows (trace empty).
     std::vector<BfsOutcome> run_batch(const uint32_t* srcs, uint32_t count, const EngineOptions& opt,
                                       uint32_t* levels_host);
-    const uint32_t* levels_device() const { return levels_.p; }
+    // level array written by the last launch (run_batch alternates two buffers)
+    const uint32_t* levels_device() const { return last_levels_ ? last_levels_ : levels_.p; }
     uint32_t trace_capacity() const { return trace_cap_; }
     uint32_t last_grid_ctas() const { return last_ctas_; }
     uint32_t last_threads() const { return last_threads_; }
@@ -69,12 +77,14 @@ public:
     const DeviceBvss& bvss() const { return b_; }
 
 private:
+    void ensure_sigma();
     const DeviceBvss& b_;
     uint64_t words_ = 0, wstride_ = 0;
     uint32_t trace_cap_ = 0;
     DevBuf<uint32_t> levels_;
     DevBuf<uint32_t> levels2_;           // run_batch: second level buffer
     uint32_t* level_target_ = nullptr;   // launch(): level array written (null = levels_)
+    const uint32_t* last_levels_ = nullptr;  // level array of the last launch
     DevBuf<uint32_t> bits_;              // 3 * words_
     DevBuf<unsigned long long> q_;       // 3 * max(num_vss, 1) entries
     DevBuf<unsigned long long> ctl_;     // qlen[4], result[4]

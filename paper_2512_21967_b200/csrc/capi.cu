@@ -303,34 +303,6 @@ int blest_order_jaccard_windows(blest_graph g, uint32_t sigma, uint32_t w, uint3
     API_END
 }
 
-int blest_order_degree(blest_graph g, uint32_t* forward, int host) {
-    API_BEGIN
-    NEED(g && (forward || g->g.n == 0), "null argument");
-    const uint32_t n = g->g.n;
-    if (host) {
-        DevBuf<uint32_t> f(n ? n : 1);
-        degree_order_permutation(g->g, f.p);
-        if (n) CK(cudaMemcpy(forward, f.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
-    } else {
-        degree_order_permutation(g->g, forward);
-    }
-    API_END
-}
-
-int blest_order_hub_blocks(blest_graph g, const uint32_t* base_forward, uint32_t* forward) {
-    API_BEGIN
-    NEED(g && (forward || g->g.n == 0), "null argument");
-    const uint32_t n = g->g.n;
-    DevBuf<uint32_t> base, f(n ? n : 1);
-    if (base_forward && n) {
-        base.alloc(n);
-        CK(cudaMemcpy(base.p, base_forward, (size_t)n * 4, cudaMemcpyHostToDevice));
-    }
-    hub_block_permutation(g->g, base_forward ? base.p : nullptr, f.p);
-    if (n) CK(cudaMemcpy(forward, f.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
-    API_END
-}
-
 int blest_order_random(uint32_t n, uint64_t seed, uint32_t* forward) {
     API_BEGIN
     NEED(forward || n == 0, "null argument");
@@ -498,6 +470,14 @@ int blest_bvss_update_divergence(blest_bvss b, double* out) {
     API_END
 }
 
+int blest_tile_pull(const uint32_t* masks, const uint8_t* alpha, uint32_t count, uint32_t* counts) {
+    API_BEGIN
+    NEED((masks && alpha && counts) || !count, "null argument");
+    require_device();
+    tile_pull_device(masks, alpha, count, counts);
+    API_END
+}
+
 int blest_bvss_free(blest_bvss b) {
     API_BEGIN
     delete b;
@@ -588,6 +568,14 @@ int blest_bfs_batch(blest_bvss b, const uint32_t* srcs, uint32_t count, const bl
     const std::vector<BfsOutcome> r = b->eng().run_batch(srcs, count, to_opts(cfg), levels_out);
     if (counters)
         for (uint32_t k = 0; k < count; ++k) fill_counters(r[k], counters + k, nullptr, 0);
+    API_END
+}
+
+int blest_bfs_prepare(blest_bvss b, const blest_engine_config* cfg, uint64_t* engine_bytes) {
+    API_BEGIN
+    NEED(b, "null bvss");
+    const uint64_t bytes = b->eng().prepare(to_opts(cfg));
+    if (engine_bytes) *engine_bytes = bytes;
     API_END
 }
 

@@ -175,9 +175,16 @@ __global__ void k_permute_keys(const uint64_t* __restrict__ off, const uint32_t*
 DeviceGraph graph_from_csr(uint32_t n, const uint64_t* off, const uint32_t* tgt, bool directed,
                            bool host_ptrs) {
     cudaStream_t st = stream();
-    uint64_t m = 0;
-    if (host_ptrs) m = off[n];
-    else CK(cudaMemcpy(&m, off + n, 8, cudaMemcpyDeviceToHost));
+    uint64_t m = 0, first = 0;
+    if (host_ptrs) {
+        m = off[n];
+        first = off[0];
+    } else {
+        CK(cudaMemcpy(&m, off + n, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&first, off, 8, cudaMemcpyDeviceToHost));
+    }
+    // offsets[0] must be 0: otherwise keys[0, off[0]) would never be written
+    if (first != 0) throw InvalidArgument("CSR offsets[0] must be 0");
     DevBuf<uint64_t> doff;
     DevBuf<uint32_t> dtgt;
     const uint64_t* o = off;
@@ -370,91 +377,3 @@ void graph_out_degrees(const DeviceGraph& g, uint32_t* deg_dev) {
 
 }  // namespace blestgpu
 
-namespace blestgpu {
-namespace {
-__global__ void k_degree_keys(const uint64_t* __restrict__ off, uint32_t n, uint64_t* __restrict__ keys) {
-    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t d = off[u + 1] - off[u];
-        const uint32_t inv = d >= 0xFFFFFFFFull ? 0u : (uint32_t)(0xFFFFFFFFull - d);
-        keys[u] = ((uint64_t)inv << 32) | u;
-    }
-}
-__global__ void k_rank_from_keys(const uint64_t* __restrict__ keys, uint32_t n, uint32_t* __restrict__ fwd) {
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
-        fwd[(uint32_t)keys[p]] = (uint32_t)p;
-}
-}  // namespace
-
-// Hub-first pre-pass: new id = rank by (out-degree descending, id ascending). Composed in
-// front of the Jaccard windows it keeps the windows' clustering while placing the most
-// frequently hit rows in a contiguous id prefix (the BFS kernel caches their visited bits
-// in shared memory on dense levels).
-void degree_order_permutation(const DeviceGraph& g, uint32_t* forward_dev) {
-    if (!g.n) return;
-    DevBuf<uint64_t> keys(g.n);
-    k_degree_keys<<<grid_for(g.n, 256), 256, 0, stream()>>>(g.off.p, g.n, keys.p);
-    CK(cudaGetLastError());
-    sort_keys(keys, g.n, 64);
-    k_rank_from_keys<<<grid_for(g.n, 256), 256, 0, stream()>>>(keys.p, g.n, forward_dev);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(stream()));
-}
-}  // namespace blestgpu
-
-namespace blestgpu {
-namespace {
-__global__ void k_permuted_degrees(const uint64_t* __restrict__ off, uint32_t n, const uint32_t* __restrict__ base,
-                                   uint32_t* __restrict__ deg_new) {
-    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t d = off[u + 1] - off[u];
-        deg_new[base ? base[u] : u] = d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d;
-    }
-}
-__global__ void k_block_keys(const uint32_t* __restrict__ deg, uint32_t nblocks, uint64_t* __restrict__ keys) {
-    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nblocks; b += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t s = 0;
-        for (int j = 0; j < 8; ++j) s += deg[8 * b + j];
-        const uint32_t inv = s >= 0xFFFFFFFFull ? 0u : (uint32_t)(0xFFFFFFFFull - s);
-        keys[b] = ((uint64_t)inv << 32) | b;
-    }
-}
-__global__ void k_block_forward(const uint64_t* __restrict__ keys_sorted, uint32_t nblocks, uint32_t n,
-                                const uint32_t* __restrict__ base, uint32_t* __restrict__ newpos,
-                                uint32_t* __restrict__ fwd) {
-    // newpos[old block] = rank; then forward[u] = newpos[base[u] / 8] * 8 + base[u] % 8
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nblocks; p += (uint64_t)gridDim.x * blockDim.x)
-        newpos[(uint32_t)keys_sorted[p]] = (uint32_t)p;
-}
-__global__ void k_block_compose(uint32_t nblocks, uint32_t n, const uint32_t* __restrict__ base,
-                                const uint32_t* __restrict__ newpos, uint32_t* __restrict__ fwd) {
-    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t x = base ? base[u] : (uint32_t)u;
-        const uint32_t b = x >> 3;
-        fwd[u] = (b < nblocks) ? (newpos[b] << 3 | (x & 7)) : x;  // partial tail block stays last
-    }
-}
-}  // namespace
-
-// Hub-block post-pass: keep every 8-id slice-set block intact (so the BVSS slice sets —
-// and with them compression and the VSS dequeue count — are unchanged) but order the
-// blocks by descending degree sum. The rows hit most often by the pull then sit in a
-// compact id prefix whose visited bits stay resident in L1 (or in shared memory).
-// `base` (device, may be null) is the permutation already applied; returns the composition.
-void hub_block_permutation(const DeviceGraph& g, const uint32_t* base_dev, uint32_t* forward_dev) {
-    const uint32_t n = g.n;
-    if (!n) return;
-    const uint32_t nblocks = n / 8;
-    DevBuf<uint32_t> deg(n), newpos(nblocks ? nblocks : 1);
-    DevBuf<uint64_t> keys(nblocks ? nblocks : 1);
-    cudaStream_t st = stream();
-    k_permuted_degrees<<<grid_for(n, 256), 256, 0, st>>>(g.off.p, n, base_dev, deg.p);
-    if (nblocks) {
-        k_block_keys<<<grid_for(nblocks, 256), 256, 0, st>>>(deg.p, nblocks, keys.p);
-        sort_keys(keys, nblocks, 64);
-        k_block_forward<<<grid_for(nblocks, 256), 256, 0, st>>>(keys.p, nblocks, n, base_dev, newpos.p, forward_dev);
-    }
-    k_block_compose<<<grid_for(n, 256), 256, 0, st>>>(nblocks, n, base_dev, newpos.p, forward_dev);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
-}
-}  // namespace blestgpu

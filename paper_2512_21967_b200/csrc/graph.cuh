@@ -44,13 +44,6 @@ DeviceGraph graph_transpose(const DeviceGraph& g);
 // Seeded relabel permutation: forward[i] = rank of (hash64(seed, i), i).
 void relabel_permutation(uint32_t n, uint64_t seed, uint32_t* forward_dev);
 
-// Hub-first pre-pass: forward[u] = rank of (out-degree desc, id asc).
-void degree_order_permutation(const DeviceGraph& g, uint32_t* forward_dev);
-
-// Hub-block post-pass: 8-id blocks (under `base`, may be null) sorted by descending
-// degree sum, ids inside a block kept; forward = composition.
-void hub_block_permutation(const DeviceGraph& g, const uint32_t* base_dev, uint32_t* forward_dev);
-
 // Out-degree array (uint32, n entries) on device.
 void graph_out_degrees(const DeviceGraph& g, uint32_t* deg_dev);
 

@@ -251,6 +251,9 @@ def test_auto_pipeline_maps_levels_back(oracle):
     {"BLEST_LAZY_RECHECK": "1"},           # lazy: test V_curr, re-check V_next at L2
     {"BLEST_DENSE_MIN": "1"},              # eager: F_next re-check on every level; lazy: queue + barrier on every level
     {"BLEST_DENSE_MIN": "1000000000"},     # eager: never (straight to the atomic); lazy: every level expanded inside stage 1
+    {"BLEST_DENSE_MIN": "1", "BLEST_TAIL_DIV": "2"},  # lazy: dense levels, last half handed out dynamically
+    {"BLEST_DENSE_MIN": "1", "BLEST_TAIL_DIV": "0"},  # lazy: dense levels, static round-robin only
+    {"BLEST_LAZY_VARIANT": "tma"},         # lazy: TMA producer/consumer stage 1 (ablation)
 ])
 def test_engine_phase_variants(oracle, monkeypatch, env):
     """The batch-wide visited-test phases, the lazy σ view and their switches change only how

@@ -23,13 +23,11 @@ def main():
     ap.add_argument("--sources", type=int, default=3)
     ap.add_argument("--grid-ctas", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
-    ap.add_argument("--prepass", default="none")
-    ap.add_argument("--postpass", default="none")
     args = ap.parse_args()
     import bench
     import paper_2512_21967_b200 as B
     from paper_2512_21967_b200 import _lib as L
-    prep = bench.prepare(args.config, args.order, 1 << 16, args.prepass, args.postpass)
+    prep = bench.prepare(args.config, args.order, 1 << 16)
     b, g, plan, perm = prep["b"], prep["g"], prep["plan"], prep["perm"]
     mode = B.choose_mode(b, plan, B.EngineConfig(mode=B.engine_mode_from_string(args.mode)))
     lib = L.lib()
