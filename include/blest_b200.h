@@ -33,6 +33,7 @@ extern "C" {
 #define BLEST_ELOGIC (-3)
 #define BLEST_ECUDA (-4)
 #define BLEST_ENOMEM (-5)
+#define BLEST_EPARSE (-6) /* blest::ParseError (R:include/blest/graph.hpp:23-32), a runtime_error */
 
 typedef struct blest_graph_s* blest_graph; /* device CSR out-view (blest::Graph, R:include/blest/graph.hpp:38-79) */
 typedef struct blest_bvss_s* blest_bvss;   /* device BVSS + BFS workspace (blest::Bvss, R:include/blest/bvss.hpp:34-63) */
@@ -81,6 +82,21 @@ int blest_graph_out_degrees(blest_graph g, uint32_t* deg, int host);
  * (the GTEPS numerator); levels in device memory. */
 int blest_graph_traversed_edges(blest_graph g, const uint32_t* levels_dev, uint64_t* edges);
 int blest_graph_free(blest_graph g);
+/* in_offsets()/in_sources() (R:include/blest/graph.hpp:58-68): the incoming view (transpose on
+ * the device) copied into host arrays (offsets[n+1], sources[m]). */
+int blest_graph_copy_in_csr(blest_graph g, uint64_t* offsets, uint32_t* sources);
+/* Graph::digest (R:include/blest/graph.hpp:70-71, R:src/graph.cpp:62-75): FNV-1a over
+ * (n, m, arc list) — the BVSS cache key. */
+int blest_graph_digest(blest_graph g, uint64_t* digest);
+/* reference_bfs (R:include/blest/graph.hpp:119, R:src/graph.cpp:144-167) on the device: a
+ * top-down BFS straight over the CSR (no BVSS) — the validation oracle the CLI's --validate
+ * uses. levels_out: host, n entries. */
+int blest_graph_bfs(blest_graph g, uint32_t src, uint32_t* levels_out, uint32_t* visited_count,
+                    uint32_t* num_levels);
+/* load_graph (R:include/blest/graph.hpp:150, R:src/graph.cpp:390-394): ".mtx" -> Matrix Market
+ * coordinate (pattern/real/integer, general/symmetric), else a SNAP-style edge list ("# Nodes:"
+ * directive honoured). Parse failures: BLEST_EPARSE (message carries the line number). */
+int blest_graph_load(const char* path, blest_graph* out);
 
 /* ---- ordering (R:include/blest/ordering.hpp) --------------------------------------------- */
 typedef struct {
@@ -131,6 +147,24 @@ int blest_bvss_stats(blest_bvss b, blest_bvss_stats_t* out);
 /* update_divergence alone (R:src/bvss.cpp:109-141), bit-exact with the reference. */
 int blest_bvss_update_divergence(blest_bvss b, double* out);
 int blest_bvss_free(blest_bvss b);
+/* save_bvss / load_bvss (R:include/blest/bvss.hpp:106-111, R:src/bvss.cpp:250-295): the
+ * reference's binary cache ('BVSS' magic, version 1, little-endian u32 words: sigma, tau, n,
+ * m lo/hi, numVSS, realPtrs, virtualToReal, rowIds, masks) — files are interchangeable with
+ * the reference's. Errors: BLEST_ERUNTIME (cannot open, bad magic/version, truncated,
+ * corrupt realPtrs), BLEST_EINVAL (sigma != 8). */
+int blest_bvss_save(blest_bvss b, const char* path);
+int blest_bvss_load(const char* path, blest_bvss* out);
+/* save_permutation / load_permutation (R:src/graph.cpp:396-417): one inverse id per line.
+ * load: call with forward == NULL to get *n, then with a forward[*n] array. */
+int blest_permutation_save(const uint32_t* forward, uint32_t n, const char* path);
+int blest_permutation_load(const char* path, uint32_t* forward, uint32_t* n);
+/* validate_roundtrip (R:include/blest/bvss.hpp:80-82, R:src/bvss.cpp:143-188) on the device. */
+typedef struct {
+    uint64_t checked_slices;
+    uint64_t padded_nonzero_mask, real_zero_mask, mask_bit_beyond_n, rows_mismatched;
+    uint64_t first_padded_nonzero_vss, first_zero_mask_vss, first_beyond_set, first_mismatched_row;
+} blest_roundtrip_report;
+int blest_bvss_validate_roundtrip(blest_bvss b, blest_graph g, blest_roundtrip_report* out);
 
 /* ---- BFS (R:include/blest/bfs_engine.hpp) --------------------------------------------- */
 /* EngineConfig (R:include/blest/bfs_engine.hpp:19-25) plus device knobs. */

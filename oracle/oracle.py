@@ -158,6 +158,12 @@ def ref():
                                            C.POINTER(C.c_uint32)]
         L.ref_tile_pull.argtypes = [_u32p, C.c_uint8, C.c_uint, _u32p]
         L.ref_rng_next_below.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u64p]
+        L.ref_save_bvss.argtypes = [vp, C.c_char_p]
+        L.ref_load_bvss.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.ref_save_permutation.argtypes = [_u32p, C.c_uint32, C.c_char_p]
+        L.ref_load_permutation.argtypes = [C.c_char_p, _u32p, C.c_uint32, C.POINTER(C.c_uint32)]
+        L.ref_load_graph.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.ref_validate_roundtrip.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
         _ref = L
     return _ref
 
@@ -756,3 +762,41 @@ def classify(g: Csr) -> dict:
     power = len(pts) >= 3 and -3.5 <= slope <= -1.5 and r2 >= 0.8
     rep["is_social_like"] = bool(heavy or power)
     return rep
+
+
+# ---- the reference's file formats (R:src/bvss.cpp:218-295, R:src/graph.cpp:233-417) ----
+def ref_save_bvss(b: "RefBvss", path: str) -> None:
+    _chk(ref().ref_save_bvss(b.ptr, os.fsencode(path)))
+
+
+def ref_load_bvss(path: str) -> "RefBvss":
+    out = C.c_void_p()
+    _chk(ref().ref_load_bvss(os.fsencode(path), C.byref(out)))
+    return RefBvss(out.value)
+
+
+def ref_save_permutation(forward, path: str) -> None:
+    f = np.ascontiguousarray(forward, np.uint32)
+    _chk(ref().ref_save_permutation(f if len(f) else np.zeros(1, np.uint32), len(f), os.fsencode(path)))
+
+
+def ref_load_permutation(path: str, cap: int = 1 << 24) -> np.ndarray:
+    f = np.zeros(cap, np.uint32)
+    n = C.c_uint32()
+    _chk(ref().ref_load_permutation(os.fsencode(path), f, cap, C.byref(n)))
+    return f[: n.value].copy()
+
+
+def ref_load_graph(path: str) -> RefGraph:
+    out = C.c_void_p()
+    _chk(ref().ref_load_graph(os.fsencode(path), C.byref(out)))
+    return RefGraph(out.value)
+
+
+def ref_validate_roundtrip(b: "RefBvss", g: RefGraph):
+    """(#discrepancies, checked_slices) of the reference's validate_roundtrip."""
+    checked = C.c_uint64()
+    r = ref().ref_validate_roundtrip(b.ptr, g.ptr, C.byref(checked))
+    if r < 0:
+        raise RefError(r, ref().ref_last_error().decode())
+    return r, checked.value

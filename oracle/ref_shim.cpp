@@ -252,6 +252,42 @@ int ref_check_bvss_invariants(const void* b, const void* g) {
             .size());
 }
 
+// save_bvss / load_bvss (R:src/bvss.cpp:250-295)
+int ref_save_bvss(const void* b, const char* path) {
+    GUARD({ save_bvss(*static_cast<const Bvss*>(b), path); })
+}
+int ref_load_bvss(const char* path, void** out) {
+    GUARD({ *out = new Bvss(load_bvss(path)); })
+}
+
+// save_permutation / load_permutation (R:src/graph.cpp:396-417): forward maps
+int ref_save_permutation(const uint32_t* forward, uint32_t n, const char* path) {
+    GUARD({ save_permutation(Permutation::from_forward(std::vector<VertexId>(forward, forward + n)), path); })
+}
+int ref_load_permutation(const char* path, uint32_t* forward, uint32_t cap, uint32_t* n) {
+    GUARD({
+        const Permutation p = load_permutation(path);
+        *n = p.size();
+        for (uint32_t i = 0; i < p.size() && i < cap; ++i) forward[i] = p.forward(i);
+    })
+}
+
+// load_graph (R:src/graph.cpp:390-394)
+int ref_load_graph(const char* path, void** out) {
+    GUARD({ *out = new Graph(load_graph(path)); })
+}
+
+// validate_roundtrip (R:src/bvss.cpp:143-188): number of discrepancies
+int ref_validate_roundtrip(const void* b, const void* g, uint64_t* checked) {
+    try {
+        const RoundtripReport r = validate_roundtrip(*static_cast<const Bvss*>(b), *static_cast<const Graph*>(g));
+        *checked = r.checked_slices;
+        return static_cast<int>(r.discrepancies.size());
+    } catch (const std::exception& e) {
+        return -fail(e) - 100;
+    }
+}
+
 // ---- engines (R:src/bfs_engine.cpp) ---------------------------------------------
 // trace_out rows (8 u64 per level): level, queue_size, frontier_population, discovered,
 // full_atomics, stage1_full_atomics, relaxed_atomics, queue_pushes.

@@ -8,5 +8,7 @@ from .api import (  # noqa: F401
     build_bvss, bvss_stats, choose_mode, classify_social_like, compression_ratio, device_info,
     engine_mode_from_string, init_state, jaccard_with_windows, make_permutation,
     ordering_strategy_from_string, prepare, random_order, rcm, relabel_permutation, run_auto,
-    run_auto_prebuilt, run_batch, run_eager, run_lazy, select_plan, update_divergence)
-from ._lib import BlestCudaError, BlestLogicError, LIB_PATH  # noqa: F401
+    run_auto_prebuilt, run_batch, run_eager, run_lazy, select_plan, update_divergence,
+    RoundtripReport, load_bvss, load_graph, load_permutation, reference_bfs, save_bvss,
+    save_permutation, tile_pull, validate_roundtrip)
+from ._lib import BlestCudaError, BlestLogicError, LIB_PATH, ParseError  # noqa: F401

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BLEST_LIB") or os.path.join(HERE, "libblest_b200.so")
 
 BLEST_OK, BLEST_EINVAL, BLEST_ERUNTIME, BLEST_ELOGIC, BLEST_ECUDA, BLEST_ENOMEM = 0, -1, -2, -3, -4, -5
+BLEST_EPARSE = -6
 MODE_EAGER, MODE_LAZY, MODE_AUTO = 0, 1, 2
 PULL_POPC, PULL_MMA = 0, 1
 
@@ -31,6 +32,24 @@ class BlestCudaError(BlestError, RuntimeError):
 
 class BlestLogicError(BlestError, AssertionError):
     """std::logic_error: an engine invariant broke."""
+
+
+class ParseError(RuntimeError):
+    """blest::ParseError (R:include/blest/graph.hpp:23-32): a runtime_error with a line."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        import re
+        m = re.search(r"\(line (\d+)\)$", msg)
+        self.line = int(m.group(1)) if m else 0
+
+
+class RoundtripReportT(C.Structure):
+    _fields_ = [("checked_slices", C.c_uint64), ("padded_nonzero_mask", C.c_uint64),
+                ("real_zero_mask", C.c_uint64), ("mask_bit_beyond_n", C.c_uint64),
+                ("rows_mismatched", C.c_uint64), ("first_padded_nonzero_vss", C.c_uint64),
+                ("first_zero_mask_vss", C.c_uint64), ("first_beyond_set", C.c_uint64),
+                ("first_mismatched_row", C.c_uint64)]
 
 
 class BvssInfo(C.Structure):
@@ -115,6 +134,15 @@ SIGNATURES = {
     "blest_bfs_batch": (i32, [vp, vp, u32, P(EngineConfigT), vp, vp]),
     "blest_bfs_prepare": (i32, [vp, vp, P(u64)]),
     "blest_tile_pull": (i32, [vp, vp, u32, vp]),
+    "blest_graph_copy_in_csr": (i32, [vp, vp, vp]),
+    "blest_graph_digest": (i32, [vp, P(u64)]),
+    "blest_graph_bfs": (i32, [vp, u32, vp, P(u32), P(u32)]),
+    "blest_graph_load": (i32, [C.c_char_p, P(vp)]),
+    "blest_bvss_save": (i32, [vp, C.c_char_p]),
+    "blest_bvss_load": (i32, [C.c_char_p, P(vp)]),
+    "blest_permutation_save": (i32, [vp, u32, C.c_char_p]),
+    "blest_permutation_load": (i32, [C.c_char_p, vp, P(u32)]),
+    "blest_bvss_validate_roundtrip": (i32, [vp, vp, P(RoundtripReportT)]),
     "blest_bfs_levels_device": (i32, [vp, P(vp)]),
     "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),
@@ -165,4 +193,6 @@ def check(rc: int) -> None:
         raise BlestLogicError(rc, msg)
     if rc == BLEST_ENOMEM:
         raise MemoryError(msg)
+    if rc == BLEST_EPARSE:
+        raise ParseError(msg)
     raise BlestCudaError(rc, msg)

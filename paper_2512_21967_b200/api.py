@@ -1,9 +1,13 @@
 """Python mirror of the reference's C++ API for the hot path (R = /root/reference/proj):
 
-    graph load   Graph.from_edges / Graph.from_csr         R:include/blest/graph.hpp:38-79
+    graph load   Graph.from_edges / Graph.from_csr /      R:include/blest/graph.hpp:38-79, :150
+                 load_graph, Graph.digest / in_* views,
+                 reference_bfs (device, over the CSR)     R:include/blest/graph.hpp:119
     reorder      select_plan / make_permutation / rcm /   R:include/blest/ordering.hpp:12-83
                  jaccard_with_windows / apply_permutation
-    BVSS build   build_bvss / bvss_stats                   R:include/blest/bvss.hpp:16-111
+    BVSS build   build_bvss / bvss_stats / save_bvss /    R:include/blest/bvss.hpp:16-111
+                 load_bvss / validate_roundtrip,
+                 save_permutation / load_permutation      R:src/graph.cpp:396-417
     bfs(source)  run_eager / run_lazy / run_auto_prebuilt  R:include/blest/bfs_engine.hpp:14-101
                  / run_auto
 
@@ -16,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -134,6 +139,54 @@ class Graph:
         e = C.c_uint64()
         L.check(L.lib().blest_graph_traversed_edges(self._h, levels_device_ptr, C.byref(e)))
         return e.value
+
+    # the incoming view (R:include/blest/graph.hpp:54-68): transposed on the device, cached
+    def in_csr(self):
+        if getattr(self, "_in", None) is None:
+            off = np.zeros(self._n + 1, np.uint64)
+            src = np.zeros(max(self._m, 1), np.uint32)
+            L.check(L.lib().blest_graph_copy_in_csr(self._h, _ptr(off), _ptr(src)))
+            self._in = (off, src[: self._m])
+        return self._in
+
+    def in_offsets(self) -> np.ndarray:
+        return self.in_csr()[0]
+
+    def in_sources(self) -> np.ndarray:
+        return self.in_csr()[1]
+
+    def in_neighbors(self, v: int) -> np.ndarray:
+        off, src = self.in_csr()
+        return src[int(off[v]): int(off[v + 1])]
+
+    def in_degree(self, v: int) -> int:
+        off = self.in_csr()[0]
+        return int(off[v + 1] - off[v])
+
+    def out_neighbors(self, u: int) -> np.ndarray:
+        off, tgt = self._host_csr()
+        return tgt[int(off[u]): int(off[u + 1])]
+
+    def out_degree(self, u: int) -> int:
+        off = self._host_csr()[0]
+        return int(off[u + 1] - off[u])
+
+    def has_edge(self, u: int, v: int) -> bool:
+        """Graph::has_edge (R:src/graph.cpp:57-60): binary search in u's sorted out-list."""
+        nb = self.out_neighbors(u)
+        i = int(np.searchsorted(nb, v))
+        return i < len(nb) and int(nb[i]) == v
+
+    def _host_csr(self):
+        if getattr(self, "_out", None) is None:
+            self._out = self.csr()
+        return self._out
+
+    def digest(self) -> int:
+        """Graph::digest (R:src/graph.cpp:62-75): FNV-1a over (n, m, arcs), the cache key."""
+        d = C.c_uint64()
+        L.check(L.lib().blest_graph_digest(self._h, C.byref(d)))
+        return d.value
 
     def pick_sources(self, count: int, seed: int, skip_isolated: bool = True) -> np.ndarray:
         out = np.zeros(max(count, 1), np.uint32)
@@ -405,6 +458,79 @@ class Bvss:
             L.check(L.lib().blest_bvss_update_divergence(self._h, C.byref(d)))
             self._divergence = d.value
         return self._divergence
+
+
+def save_bvss(b: Bvss, path: str) -> None:
+    """save_bvss (R:src/bvss.cpp:250-266): the reference's 'BVSS' v1 binary cache."""
+    L.check(L.lib().blest_bvss_save(b.handle, os.fsencode(path)))
+
+
+def load_bvss(path: str) -> Bvss:
+    """load_bvss (R:src/bvss.cpp:268-295)."""
+    out = C.c_void_p()
+    L.check(L.lib().blest_bvss_load(os.fsencode(path), C.byref(out)))
+    return Bvss(out.value)
+
+
+def save_permutation(p: Permutation, path: str) -> None:
+    """save_permutation (R:src/graph.cpp:396-401): one inverse id per line."""
+    f = p.forward_map()
+    L.check(L.lib().blest_permutation_save(_ptr(f), len(f), os.fsencode(path)))
+
+
+def load_permutation(path: str) -> Permutation:
+    """load_permutation (R:src/graph.cpp:403-417)."""
+    n = C.c_uint32(0)
+    L.check(L.lib().blest_permutation_load(os.fsencode(path), None, C.byref(n)))
+    f = np.zeros(max(n.value, 1), np.uint32)
+    L.check(L.lib().blest_permutation_load(os.fsencode(path), _ptr(f), C.byref(n)))
+    return Permutation(f[: n.value])
+
+
+def load_graph(path: str) -> Graph:
+    """load_graph (R:src/graph.cpp:390-394): .mtx Matrix Market, else an edge list."""
+    out = C.c_void_p()
+    L.check(L.lib().blest_graph_load(os.fsencode(path), C.byref(out)))
+    return Graph(out.value)
+
+
+def reference_bfs(g: Graph, src: int) -> "BfsResult":
+    """reference_bfs (R:src/graph.cpp:144-167), on the device straight over the CSR (the
+    validation oracle the CLI's --validate compares the engines with)."""
+    if not 0 <= int(src) < g.num_vertices():
+        raise ValueError("bfs source out of range")
+    lv = np.zeros(max(g.num_vertices(), 1), np.uint32)
+    vis, nl = C.c_uint32(), C.c_uint32()
+    L.check(L.lib().blest_graph_bfs(g.handle, int(src), _ptr(lv), C.byref(vis), C.byref(nl)))
+    return BfsResult(source=int(src), levels=lv[: g.num_vertices()], visited_count=vis.value,
+                     num_levels=nl.value)
+
+
+@dataclass
+class RoundtripReport:
+    checked_slices: int = 0
+    discrepancies: list = field(default_factory=list)
+
+    def ok(self) -> bool:
+        return not self.discrepancies
+
+
+def validate_roundtrip(b: Bvss, g: Graph) -> RoundtripReport:
+    """validate_roundtrip (R:src/bvss.cpp:143-188) on the device: every slot decoded, the
+    padding rules checked, the decoded arcs compared with g's incoming view per row. One
+    discrepancy entry per violation class (with its count and first offender)."""
+    r = L.RoundtripReportT()
+    L.check(L.lib().blest_bvss_validate_roundtrip(b.handle, g.handle, C.byref(r)))
+    d = []
+    if r.padded_nonzero_mask:
+        d.append(f"padded slot with nonzero mask at vss {r.first_padded_nonzero_vss} ({r.padded_nonzero_mask} slots)")
+    if r.real_zero_mask:
+        d.append(f"real slot with zero mask at vss {r.first_zero_mask_vss} ({r.real_zero_mask} slots)")
+    if r.mask_bit_beyond_n:
+        d.append(f"mask bit beyond n at slice set {r.first_beyond_set} ({r.mask_bit_beyond_n} bits)")
+    if r.rows_mismatched:
+        d.append(f"incoming list mismatch at row {r.first_mismatched_row} ({r.rows_mismatched} rows)")
+    return RoundtripReport(int(r.checked_slices), d)
 
 
 def build_bvss(g: Graph) -> Bvss:

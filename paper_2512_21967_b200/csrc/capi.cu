@@ -10,6 +10,7 @@
 #include "bfs.cuh"
 #include "bvss.cuh"
 #include "graph.cuh"
+#include "io.cuh"
 #include "ordering.cuh"
 
 using namespace blestgpu;
@@ -97,6 +98,7 @@ void require_device() {
     return BLEST_OK;                                                         \
     }                                                                        \
     catch (const InvalidArgument& e) { return fail_with(BLEST_EINVAL, e.what()); } \
+    catch (const ParseError& e) { return fail_with(BLEST_EPARSE, e.what()); }      \
     catch (const RuntimeError& e) { return fail_with(BLEST_ERUNTIME, e.what()); }  \
     catch (const LogicError& e) { return fail_with(BLEST_ELOGIC, e.what()); }      \
     catch (const CudaError& e) { return fail_with(BLEST_ECUDA, e.what()); }        \
@@ -271,6 +273,48 @@ int blest_graph_free(blest_graph g) {
     API_END
 }
 
+int blest_graph_copy_in_csr(blest_graph g, uint64_t* offsets, uint32_t* sources) {
+    API_BEGIN
+    NEED(g && offsets && (sources || g->g.m == 0), "null argument");
+    const DeviceGraph t = graph_transpose(g->g);
+    CK(cudaMemcpy(offsets, t.off.p, ((size_t)t.n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (t.m) CK(cudaMemcpy(sources, t.tgt.p, t.m * 4, cudaMemcpyDeviceToHost));
+    API_END
+}
+
+int blest_graph_digest(blest_graph g, uint64_t* digest) {
+    API_BEGIN
+    NEED(g && digest, "null argument");
+    *digest = graph_digest(g->g);
+    API_END
+}
+
+int blest_graph_bfs(blest_graph g, uint32_t src, uint32_t* levels_out, uint32_t* visited_count,
+                    uint32_t* num_levels) {
+    API_BEGIN
+    NEED(g, "null graph");
+    DevBuf<uint32_t> L(g->g.n ? g->g.n : 1);
+    uint32_t nl = 0;
+    const uint32_t vis = graph_bfs_levels(g->g, src, L.p, &nl);
+    if (levels_out && g->g.n) CK(cudaMemcpy(levels_out, L.p, (size_t)g->g.n * 4, cudaMemcpyDeviceToHost));
+    if (visited_count) *visited_count = vis;
+    if (num_levels) *num_levels = nl;
+    API_END
+}
+
+int blest_graph_load(const char* path, blest_graph* out) {
+    API_BEGIN
+    NEED(path && out, "null argument");
+    const std::string p(path);
+    require_device();
+    const LoadedEdges e = (p.size() >= 4 && p.compare(p.size() - 4, 4, ".mtx") == 0) ? load_matrix_market(p)
+                                                                                    : load_edge_list(p);
+    auto h = std::make_unique<blest_graph_s>();
+    h->g = graph_from_edges(e.n, e.src.data(), e.dst.data(), e.src.size(), e.directed, true);
+    *out = h.release();
+    API_END
+}
+
 // ---- ordering ---------------------------------------------------------------------------
 int blest_classify_social_like(blest_graph g, blest_social_report* out) {
     API_BEGIN
@@ -340,6 +384,58 @@ int blest_bvss_build(blest_graph g, blest_bvss* out) {
     auto h = std::make_unique<blest_bvss_s>();
     h->b = bvss_build(g->g);
     *out = h.release();
+    API_END
+}
+
+int blest_bvss_save(blest_bvss b, const char* path) {
+    API_BEGIN
+    NEED(b && path, "null argument");
+    bvss_save(b->b, path);
+    API_END
+}
+
+int blest_bvss_load(const char* path, blest_bvss* out) {
+    API_BEGIN
+    NEED(path && out, "null argument");
+    require_device();
+    auto h = std::make_unique<blest_bvss_s>();
+    h->b = bvss_load(path);
+    *out = h.release();
+    API_END
+}
+
+int blest_permutation_save(const uint32_t* forward, uint32_t n, const char* path) {
+    API_BEGIN
+    NEED((forward || n == 0) && path, "null argument");
+    permutation_save(forward, n, path);
+    API_END
+}
+
+int blest_permutation_load(const char* path, uint32_t* forward, uint32_t* n) {
+    API_BEGIN
+    NEED(path && n, "null argument");
+    const std::vector<uint32_t> f = permutation_load(path);
+    if (forward) {
+        NEED(*n >= f.size(), "forward array too small");
+        std::memcpy(forward, f.data(), f.size() * 4);
+    }
+    *n = (uint32_t)f.size();
+    API_END
+}
+
+int blest_bvss_validate_roundtrip(blest_bvss b, blest_graph g, blest_roundtrip_report* out) {
+    API_BEGIN
+    NEED(b && g && out, "null argument");
+    const RoundtripCounts r = bvss_validate_roundtrip(b->b, g->g);
+    out->checked_slices = r.checked_slices;
+    out->padded_nonzero_mask = r.padded_nonzero;
+    out->real_zero_mask = r.real_zero_mask;
+    out->mask_bit_beyond_n = r.beyond_n;
+    out->rows_mismatched = r.rows_mismatched;
+    out->first_padded_nonzero_vss = r.first_padded_nonzero_vss;
+    out->first_zero_mask_vss = r.first_zero_mask_vss;
+    out->first_beyond_set = r.first_beyond_set;
+    out->first_mismatched_row = r.first_mismatched_row;
     API_END
 }
 

@@ -68,6 +68,8 @@ void sort_keys(DevBuf<uint64_t>& keys, uint64_t k, int end_bit) {
 
 }  // namespace
 
+void sort_keys_u64(DevBuf<uint64_t>& keys, uint64_t k, int end_bit) { sort_keys(keys, k, end_bit); }
+
 DeviceGraph graph_from_keys(uint32_t n, DevBuf<uint64_t>& keys, uint64_t k, bool directed) {
     cudaStream_t st = stream();
     uint64_t total = k;

@@ -38,6 +38,9 @@ DeviceGraph graph_generate_rmat(uint32_t scale, uint64_t num_edges, uint64_t see
 DeviceGraph graph_generate_urand(uint32_t n, uint64_t num_edges, uint64_t seed);
 DeviceGraph graph_generate_grid(uint32_t rows, uint32_t cols);
 
+// CUB radix sort of k u64 keys on bits [0, end_bit) (keys may be swapped with a new buffer).
+void sort_keys_u64(DevBuf<uint64_t>& keys, uint64_t k, int end_bit);
+
 // transpose (R:src/graph.cpp:136-142)
 DeviceGraph graph_transpose(const DeviceGraph& g);
 
