@@ -32,6 +32,11 @@ clean:
 
 cpptest: tests/cpp/facade_test
 
-tests/cpp/facade_test: tests/cpp/facade_test.cpp include/blest_b200.hpp include/blest_b200.h $(LIB)
+# the facade test program takes its expected values from the compiled reference (oracle/_ref)
+tests/cpp/facade_test: tests/cpp/facade_test.cpp include/blest_b200.hpp include/blest_b200.h $(LIB) | oracle/_ref/libblest_ref.so
 	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ tests/cpp/facade_test.cpp -Lpaper_2512_21967_b200 -lblest_b200 \
-	    -Wl,-rpath,'$$ORIGIN/../../paper_2512_21967_b200'
+	    -Loracle/_ref -lblest_ref \
+	    -Wl,-rpath,'$$ORIGIN/../../paper_2512_21967_b200' -Wl,-rpath,'$$ORIGIN/../../oracle/_ref'
+
+oracle/_ref/libblest_ref.so:
+	$(MAKE) -s -C oracle ref

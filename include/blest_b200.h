@@ -82,6 +82,8 @@ int blest_graph_out_degrees(blest_graph g, uint32_t* deg, int host);
  * (the GTEPS numerator); levels in device memory. */
 int blest_graph_traversed_edges(blest_graph g, const uint32_t* levels_dev, uint64_t* edges);
 int blest_graph_free(blest_graph g);
+/* transpose (R:include/blest/graph.hpp:109, R:src/graph.cpp:136-142): every arc reversed. */
+int blest_graph_transpose(blest_graph g, blest_graph* out);
 /* in_offsets()/in_sources() (R:include/blest/graph.hpp:58-68): the incoming view (transpose on
  * the device) copied into host arrays (offsets[n+1], sources[m]). */
 int blest_graph_copy_in_csr(blest_graph g, uint64_t* offsets, uint32_t* sources);

@@ -5,6 +5,10 @@
 // the B200:
 //
 //   blest::Graph::from_edges      R:include/blest/graph.hpp:43-44    (GPU sort/unique/CSR)
+//   blest::load_graph / transpose / reference_bfs / Graph::digest / in-views
+//                                 R:include/blest/graph.hpp:54-71, :109, :119, :150
+//   blest::save_bvss / load_bvss / validate_roundtrip / save_permutation / load_permutation
+//                                 R:include/blest/bvss.hpp:80-111, R:src/graph.cpp:396-417
 //   blest::apply_permutation      R:include/blest/graph.hpp:106
 //   blest::classify_social_like / select_plan / make_permutation / rcm / jaccard_with_windows
 //   / random_order                R:include/blest/ordering.hpp:44-81
@@ -19,6 +23,7 @@
 // owns a device handle (its public host arrays are filled as in the reference).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <limits>
 #include <map>
@@ -39,11 +44,27 @@ using EdgeId = std::uint64_t;
 using Level = std::uint32_t;
 inline constexpr Level kUnreached = std::numeric_limits<Level>::max();
 
+// ParseError (R:include/blest/graph.hpp:23-32)
+class ParseError : public std::runtime_error {
+public:
+    ParseError(const std::string& what, std::size_t line = 0)
+        : std::runtime_error(what), line_(line) {}
+    std::size_t line() const { return line_; }
+
+private:
+    std::size_t line_;
+};
+
 namespace detail {
+inline std::size_t parse_line(const std::string& msg) {  // "... (line N)"
+    const auto p = msg.rfind("(line ");
+    return p == std::string::npos ? 0 : (std::size_t)std::stoull(msg.substr(p + 6));
+}
 inline void check(int rc) {
     if (rc == BLEST_OK) return;
     const std::string msg = blest_last_error();
     switch (rc) {
+        case BLEST_EPARSE: throw ParseError(msg, parse_line(msg));
         case BLEST_EINVAL: throw std::invalid_argument(msg);
         case BLEST_ELOGIC: throw std::logic_error(msg);
         case BLEST_ENOMEM: throw std::bad_alloc();
@@ -80,9 +101,25 @@ public:
     std::span<const VertexId> out_neighbors(VertexId u) const {
         return {out_targets_.data() + out_offsets_[u], out_targets_.data() + out_offsets_[u + 1]};
     }
+    std::span<const VertexId> in_neighbors(VertexId v) const {
+        return {in_sources_.data() + in_offsets_[v], in_sources_.data() + in_offsets_[v + 1]};
+    }
     EdgeId out_degree(VertexId u) const { return out_offsets_[u + 1] - out_offsets_[u]; }
+    EdgeId in_degree(VertexId v) const { return in_offsets_[v + 1] - in_offsets_[v]; }
+    bool has_edge(VertexId u, VertexId v) const {
+        const auto nb = out_neighbors(u);
+        return std::binary_search(nb.begin(), nb.end(), v);
+    }
     const std::vector<EdgeId>& out_offsets() const { return out_offsets_; }
     const std::vector<VertexId>& out_targets() const { return out_targets_; }
+    const std::vector<EdgeId>& in_offsets() const { return in_offsets_; }
+    const std::vector<VertexId>& in_sources() const { return in_sources_; }
+    // FNV-1a over (n, m, arc list); keys the on-disk caches (R:src/graph.cpp:62-75).
+    std::uint64_t digest() const {
+        std::uint64_t d = 0;
+        detail::check(blest_graph_digest(h_.get(), &d));
+        return d;
+    }
     blest_graph handle() const { return h_.get(); }
 
 private:
@@ -97,14 +134,21 @@ private:
         out_offsets_.resize((std::size_t)n + 1);
         out_targets_.resize(m);
         detail::check(blest_graph_copy_csr(h, out_offsets_.data(), out_targets_.data()));
+        in_offsets_.resize((std::size_t)n + 1);  // both views materialised, as the reference does
+        in_sources_.resize(m);
+        detail::check(blest_graph_copy_in_csr(h, in_offsets_.data(), in_sources_.data()));
     }
     friend Graph apply_permutation(const Graph&, const class Permutation&);
+    friend Graph transpose(const Graph&);
+    friend Graph load_graph(const std::string&);
     std::shared_ptr<blest_graph_s> h_;
     VertexId n_ = 0;
     EdgeId m_ = 0;
     bool directed_ = true;
     std::vector<EdgeId> out_offsets_{0};
     std::vector<VertexId> out_targets_;
+    std::vector<EdgeId> in_offsets_{0};
+    std::vector<VertexId> in_sources_;
 };
 
 class Permutation {
@@ -156,10 +200,37 @@ private:
     std::vector<VertexId> forward_, inverse_;
 };
 
+// save_permutation / load_permutation (R:src/graph.cpp:396-417): one inverse id per line.
+inline void save_permutation(const Permutation& p, const std::string& path) {
+    detail::check(blest_permutation_save(p.forward_map().data(), p.size(), path.c_str()));
+}
+
+inline Permutation load_permutation(const std::string& path) {
+    std::uint32_t n = 0;
+    detail::check(blest_permutation_load(path.c_str(), nullptr, &n));
+    std::vector<VertexId> f(n);
+    detail::check(blest_permutation_load(path.c_str(), f.data(), &n));
+    return Permutation::from_forward(std::move(f));
+}
+
 inline Graph apply_permutation(const Graph& g, const Permutation& perm) {
     if (perm.size() != g.num_vertices()) throw std::invalid_argument("permutation size does not match vertex count");
     blest_graph h = nullptr;
     detail::check(blest_graph_apply_permutation(g.handle(), perm.forward_map().data(), 1, &h));
+    return Graph(h);
+}
+
+// transpose (R:include/blest/graph.hpp:109, R:src/graph.cpp:136-142), on the device.
+inline Graph transpose(const Graph& g) {
+    blest_graph h = nullptr;
+    detail::check(blest_graph_transpose(g.handle(), &h));
+    return Graph(h);
+}
+
+// load_graph (R:include/blest/graph.hpp:150): ".mtx" Matrix Market, else an edge list.
+inline Graph load_graph(const std::string& path) {
+    blest_graph h = nullptr;
+    detail::check(blest_graph_load(path.c_str(), &h));
     return Graph(h);
 }
 
@@ -169,6 +240,20 @@ struct BfsResult {
     VertexId visited_count = 0;
     Level num_levels = 0;
 };
+
+// reference_bfs (R:include/blest/graph.hpp:119): the ground truth the engines are checked
+// against — here a top-down BFS straight over the CSR on the device (no BVSS).
+inline BfsResult reference_bfs(const Graph& g, VertexId source) {
+    BfsResult r;
+    r.source = source;
+    r.levels.resize(g.num_vertices());
+    std::uint32_t vis = 0, nl = 0;
+    detail::check(blest_graph_bfs(g.handle(), source, r.levels.data(), &vis, &nl));
+    r.visited_count = vis;
+    r.num_levels = nl;
+    return r;
+}
+
 
 // ---- ordering (R:include/blest/ordering.hpp) ------------------------------------------
 enum class OrderingStrategy { JaccardWindows, Rcm, Random, Identity };
@@ -320,6 +405,40 @@ inline Bvss build_bvss(const Graph& g, const BvssConfig& cfg = {}, unsigned work
     blest_bvss h = nullptr;
     detail::check(blest_bvss_build(g.handle(), &h));
     return Bvss::adopt(h);
+}
+
+// save_bvss / load_bvss (R:include/blest/bvss.hpp:106-111): the reference's 'BVSS' v1 file.
+inline void save_bvss(const Bvss& b, const std::string& path) {
+    detail::check(blest_bvss_save(b.handle(), path.c_str()));
+}
+inline Bvss load_bvss(const std::string& path) {
+    blest_bvss h = nullptr;
+    detail::check(blest_bvss_load(path.c_str(), &h));
+    return Bvss::adopt(h);
+}
+
+// validate_roundtrip (R:include/blest/bvss.hpp:75-82), decoded and compared on the device;
+// one discrepancy entry per violation class, naming its first offender and count.
+struct RoundtripReport {
+    std::uint64_t checked_slices = 0;
+    std::vector<std::string> discrepancies;
+    bool ok() const { return discrepancies.empty(); }
+};
+inline RoundtripReport validate_roundtrip(const Bvss& b, const Graph& g) {
+    blest_roundtrip_report r{};
+    detail::check(blest_bvss_validate_roundtrip(b.handle(), g.handle(), &r));
+    RoundtripReport out;
+    out.checked_slices = r.checked_slices;
+    auto add = [&](std::uint64_t count, const char* what, std::uint64_t first) {
+        if (count)
+            out.discrepancies.push_back(std::string(what) + std::to_string(first) + " (" + std::to_string(count) +
+                                        " in total)");
+    };
+    add(r.padded_nonzero_mask, "padded slot with nonzero mask at vss ", r.first_padded_nonzero_vss);
+    add(r.real_zero_mask, "real slot with zero mask at vss ", r.first_zero_mask_vss);
+    add(r.mask_bit_beyond_n, "mask bit beyond n at slice set ", r.first_beyond_set);
+    add(r.rows_mismatched, "incoming list mismatch at row ", r.first_mismatched_row);
+    return out;
 }
 
 inline double compression_ratio(const Bvss& b) {

@@ -135,6 +135,7 @@ SIGNATURES = {
     "blest_bfs_prepare": (i32, [vp, vp, P(u64)]),
     "blest_tile_pull": (i32, [vp, vp, u32, vp]),
     "blest_graph_copy_in_csr": (i32, [vp, vp, vp]),
+    "blest_graph_transpose": (i32, [vp, P(vp)]),
     "blest_graph_digest": (i32, [vp, P(u64)]),
     "blest_graph_bfs": (i32, [vp, u32, vp, P(u32), P(u32)]),
     "blest_graph_load": (i32, [C.c_char_p, P(vp)]),

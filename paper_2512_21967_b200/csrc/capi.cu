@@ -273,6 +273,15 @@ int blest_graph_free(blest_graph g) {
     API_END
 }
 
+int blest_graph_transpose(blest_graph g, blest_graph* out) {
+    API_BEGIN
+    NEED(g && out, "null argument");
+    auto h = std::make_unique<blest_graph_s>();
+    h->g = graph_transpose(g->g);
+    *out = h.release();
+    API_END
+}
+
 int blest_graph_copy_in_csr(blest_graph g, uint64_t* offsets, uint32_t* sources) {
     API_BEGIN
     NEED(g && offsets && (sources || g->g.m == 0), "null argument");

@@ -1,13 +1,27 @@
 // C++ drop-in test: reference-style code against include/blest_b200.hpp (every call runs on
 // the B200 through the C-ABI). Re-expresses known answers of R:tests/bfs_engine_test.cpp and
-// R:tests/bvss_test.cpp; levels are checked against a queue BFS written here (test oracle).
+// R:tests/bvss_test.cpp; expected levels, digests and structure files come from the
+// UNMODIFIED reference itself (oracle/_ref/libblest_ref.so, through its C forwarder
+// oracle/ref_shim.cpp — test infrastructure, linked only into this test program).
 #include <cstdio>
-#include <deque>
+#include <unistd.h>
+#include <fstream>
 #include <random>
 #include <stdexcept>
 #include <string>
 
 #include "blest_b200.hpp"
+
+extern "C" {  // oracle/ref_shim.cpp (the reference, R = /root/reference/proj)
+int ref_graph_from_edges(uint32_t n, const uint32_t* src, const uint32_t* dst, uint64_t k, int directed, void** out);
+void ref_graph_free(void* g);
+uint64_t ref_graph_digest(const void* g);
+int ref_reference_bfs(const void* g, uint32_t src, uint32_t* levels, uint32_t* visited, uint32_t* num_levels);
+int ref_build_bvss(const void* g, unsigned workers, void** out);
+void ref_bvss_free(void* b);
+int ref_save_bvss(const void* b, const char* path);
+int ref_load_permutation(const char* path, uint32_t* forward, uint32_t cap, uint32_t* n);
+}
 
 using namespace blest;
 
@@ -20,21 +34,25 @@ static int failures = 0;
         }                                                                    \
     } while (0)
 
-static std::vector<Level> queue_bfs(const Graph& g, VertexId s) {
-    std::vector<Level> L(g.num_vertices(), kUnreached);
-    std::deque<VertexId> q{s};
-    L[s] = 0;
-    while (!q.empty()) {
-        const VertexId u = q.front();
-        q.pop_front();
-        for (VertexId v : g.out_neighbors(u))
-            if (L[v] == kUnreached) {
-                L[v] = L[u] + 1;
-                q.push_back(v);
-            }
+// The reference's own graph over the same arc list (RAII handle on blest::Graph).
+struct RefGraph {
+    void* g = nullptr;
+    RefGraph(VertexId n, const std::vector<std::pair<VertexId, VertexId>>& e, bool directed) {
+        std::vector<uint32_t> s, d;
+        for (auto [u, v] : e) {
+            s.push_back(u);
+            d.push_back(v);
+        }
+        if (ref_graph_from_edges(n, s.data(), d.data(), e.size(), directed, &g) != 0) throw std::runtime_error("ref");
     }
-    return L;
-}
+    ~RefGraph() { ref_graph_free(g); }
+    std::vector<Level> bfs(VertexId src, VertexId n) const {  // reference_bfs (R:src/graph.cpp:144-167)
+        std::vector<Level> L(n);
+        uint32_t vis = 0, nl = 0;
+        ref_reference_bfs(g, src, L.data(), &vis, &nl);
+        return L;
+    }
+};
 
 int main() {
     EngineConfig cfg;
@@ -70,17 +88,27 @@ int main() {
             CHECK(c.trace.size() == 4 && c.trace[0].queue_pushes == 1 && c.trace[3].queue_pushes == 0);
         }
     }
-    // random directed + undirected graphs vs a queue BFS, both engines, both pulls
+    // random directed + undirected graphs vs the reference's reference_bfs, both engines,
+    // both pulls; digest, in-views and the device reference_bfs vs the reference's
     {
         std::mt19937_64 rng(7);
         for (int t = 0; t < 4; ++t) {
             const VertexId n = 500 + 137 * t;
             std::vector<std::pair<VertexId, VertexId>> e;
             for (int i = 0; i < 6 * (int)n; ++i) e.emplace_back(rng() % n, rng() % n);
-            const Graph g = Graph::from_edges(n, e, t % 2 == 0);
+            const bool directed = t % 2 == 0;
+            const Graph g = Graph::from_edges(n, e, directed);
+            const RefGraph rg(n, e, directed);
+            CHECK(g.digest() == ref_graph_digest(rg.g));
+            const Graph gt = transpose(g);
+            CHECK(gt.out_offsets() == g.in_offsets() && gt.out_targets() == g.in_sources());
+            for (VertexId u = 0; u < n; u += 97)
+                for (VertexId v : g.in_neighbors(u)) CHECK(g.has_edge(v, u));
             const Bvss b = build_bvss(g);
+            CHECK(validate_roundtrip(b, g).ok());
             for (VertexId s : {VertexId(0), VertexId(n / 2), VertexId(n - 1)}) {
-                const auto want = queue_bfs(g, s);
+                const auto want = rg.bfs(s, n);
+                CHECK(reference_bfs(g, s).levels == want);
                 for (bool lazy : {false, true})
                     for (bool mma : {false, true}) {
                         EngineConfig c2 = cfg;
@@ -91,6 +119,42 @@ int main() {
                     }
             }
         }
+    }
+    // BVSS cache + permutation files are the reference's: a file written by the reference's
+    // save_bvss loads here; our permutation file loads in the reference's load_permutation
+    {
+        std::vector<std::pair<VertexId, VertexId>> e;
+        std::mt19937_64 rng(11);
+        for (int i = 0; i < 4000; ++i) e.emplace_back(rng() % 700, rng() % 700);
+        const Graph g = Graph::from_edges(700, e, false);
+        const RefGraph rg(700, e, false);
+        void* rb = nullptr;
+        CHECK(ref_build_bvss(rg.g, 1, &rb) == 0);
+        const std::string path = "/tmp/facade_test_" + std::to_string(::getpid()) + ".bvss";
+        CHECK(ref_save_bvss(rb, path.c_str()) == 0);
+        ref_bvss_free(rb);
+        const Bvss loaded = load_bvss(path);
+        const Bvss built = build_bvss(g);
+        CHECK(loaded.row_ids == built.row_ids && loaded.masks == built.masks && loaded.real_ptrs == built.real_ptrs);
+        CHECK(run_lazy(loaded, 5, cfg).first.levels == rg.bfs(5, 700));
+        const Permutation p = random_order(700, 3);
+        save_permutation(p, path + ".perm");
+        std::vector<uint32_t> f(700);
+        uint32_t pn = 0;
+        CHECK(ref_load_permutation((path + ".perm").c_str(), f.data(), 700, &pn) == 0);
+        CHECK(pn == 700 && f == p.forward_map());
+        CHECK(load_permutation(path + ".perm").forward_map() == p.forward_map());
+        std::remove(path.c_str());
+        std::remove((path + ".perm").c_str());
+        std::ofstream(path + ".mtx") << "%%MatrixMarket matrix coordinate pattern general\n3 3 2\n1 2\n4 1\n";
+        bool threw = false;
+        try {
+            load_graph(path + ".mtx");
+        } catch (const ParseError& pe) {
+            threw = pe.line() == 4;
+        }
+        CHECK(threw);
+        std::remove((path + ".mtx").c_str());
     }
     // errors keep the reference's exception classes
     {
@@ -130,7 +194,7 @@ int main() {
         ac.ordering.window_size = 1u << 10;
         const AutoResult a = run_auto(g, 3, ac);
         CHECK(a.plan.strategy == OrderingStrategy::JaccardWindows && a.chosen_mode == EngineMode::Eager);
-        CHECK(a.bfs.levels == queue_bfs(g, 3));
+        CHECK(a.bfs.levels == RefGraph(900, e, false).bfs(3, 900));
     }
     std::printf("facade_test: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
     return failures ? 1 : 0;
