@@ -86,7 +86,7 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     const uint64_t levels_bound = (uint64_t)b.n + 2;
     trace_cap_ = (uint32_t)std::min<uint64_t>(levels_bound, 1u << 20);
     levels_.alloc(b.n ? b.n : 1);
-    wstride_ = (words_ + 3) / 4 * 4;  // 16-byte aligned bitmaps (stage 2 reads uint4)
+    wstride_ = (words_ + 1 + 3) / 4 * 4;  // 16-byte aligned bitmaps (stage 2 reads uint4) + a sentinel word
     bits_.alloc(4 * (wstride_ ? wstride_ : 4));
     q_.alloc(3 * (uint64_t)(b.num_vss ? b.num_vss : 1));
     ctl_.alloc(8);

@@ -34,55 +34,36 @@ using namespace bfsdev;
 #endif
 // Visited tests of one batch (kBatchLazy VSSs × 4 columns per lane) in batch-wide phases,
 // each phase's memory operations in flight together (one latency per phase, not one per
-// VSS): (A) for every column with a nonzero pull, the row's word of the test bitmap W —
-// a plain, L1-cached load; (B) optionally (Params::recheck) the words still clear re-read
-// from V_next at L2; (C) a fire-and-forget RED into V_next for every bit still clear
-// (legal per SURVEY §8(a) pitfall 7). Default W = V_next without (B): V_next ⊇ V_curr, so
-// a set bit means "visited before, or already marked this level", and an L1 copy lagging
-// this level's REDs from other SMs only costs an extra idempotent RED (the grid barrier
-// invalidates L1 between levels). W = V_curr with (B) is the older scheme (V_curr is
-// frozen within the level; the L2 re-check spares REDs). Measured on C2: 2.35 → 2.01 ms
-// per BFS for the default. Branch-free PTX blocks (bfs_device.cuh); rows(j) / mask(j)
-// give the lane's row ids and mask word of VSS j. Returns the number of REDs issued.
+// VSS): (A) every (VSS, column) slot's word of the test bitmap W — the row's word when the
+// lane's pull hit the column, else the sentinel word `sent` (all ones, L1-resident), so the
+// load is unconditional and needs no default move; (B) optionally (Params::recheck) the
+// words still clear re-read from V_next at L2; (C) a fire-and-forget RED into V_next for
+// every bit still clear (legal per SURVEY §8(a) pitfall 7). Default W = V_next without (B):
+// V_next ⊇ V_curr, so a set bit means "visited before, or already marked this level", and
+// an L1 copy lagging this level's REDs from other SMs only costs an extra idempotent RED
+// (the grid barrier invalidates L1 between levels). W = V_curr with (B) is the older
+// scheme (V_curr is frozen within the level; the L2 re-check spares REDs). hit[j] holds
+// the lane's 4 column hits of VSS j in bits 0..3; rw[j] its row ids. Returns the REDs
+// issued. The stage is instruction-issue bound as much as latency bound (C2 level 3:
+// ~124 warp instructions per VSS at ~74 % of the SM issue rate), so every phase is a
+// straight line of LOP3 / SHF / SEL / IMAD.WIDE / LDG|RED per slot.
 // (Codegen note: the optional phase B branch also keeps ptxas from interleaving phase
 // A's result moves with its later loads — without it the same default path measured
 // 5.3 ms per BFS.)
-template <int PULL, typename Rows, typename Mask>
-__device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t* W, uint32_t* Vn, bool recheck,
-                                                unsigned long long e, Rows rows, Mask mask) {
+template <typename Hit>
+__device__ __forceinline__ uint32_t check_batch(const uint32_t* W, uint32_t* Vn, bool recheck, uint32_t sent,
+                                                const uint4 (&rw)[kBatchLazy], Hit hit) {
     uint32_t vw[4 * kBatchLazy];
 #pragma unroll
     for (int j = 0; j < kBatchLazy; ++j) {
-        const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
-        const uint4 r = rows(j);
-        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
-        uint32_t m[4], sel[4];
-        if (PULL == 0) {  // absent entries: α = 0, no candidates
-            const uint32_t a = ej != kNoEntry ? (uint32_t)(ej >> 32) & 0xFFu : 0u;
-            const uint32_t mm = mask(j) & (a * 0x01010101u);
+        const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                m[c] = mm;
-                sel[c] = 0xFFu << (8 * c);
-            }
-        } else {
-            uint32_t cnt[4] = {0, 0, 0, 0};
-            if (ej != kNoEntry)  // warp-uniform (mma.sync needs the whole warp)
-                column_counts<PULL>(mask(j), (uint32_t)(ej >> 32) & 0xFFu, cnt);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                m[c] = cnt[c];
-                sel[c] = ~0u;
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) vw[4 * j + c] = cand_word(W, u[c], m[c], sel[c]);
+        for (int c = 0; c < 4; ++c) vw[4 * j + c] = W[hit(j, c) ? (u[c] >> 5) : sent];
     }
     if (recheck) {
 #pragma unroll
         for (int j = 0; j < kBatchLazy; ++j) {
-            const uint4 r = rows(j);
-            const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+            const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
 #pragma unroll
             for (int c = 0; c < 4; ++c) vw[4 * j + c] = recheck_word(Vn, u[c], vw[4 * j + c]);
         }
@@ -90,10 +71,17 @@ __device__ __forceinline__ uint32_t check_batch(const Params& p, const uint32_t*
     uint32_t reds = 0;
 #pragma unroll
     for (int j = 0; j < kBatchLazy; ++j) {
-        const uint4 r = rows(j);
-        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+        const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) reds += red_if_clear(Vn, u[c], vw[4 * j + c]);
+        for (int c = 0; c < 4; ++c) {
+            // ptxas never predicates a global RED (it branches around it), so the count
+            // lives inside the same branch: executed only when some lane issues the RED
+            const uint32_t bit = __funnelshift_l(0u, 1u, u[c]);
+            if (!(vw[4 * j + c] & bit)) {
+                red_or(Vn + (u[c] >> 5), bit);
+                ++reds;
+            }
+        }
     }
     return reds;
 }
@@ -134,6 +122,10 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         Vc[w] = seed;
         Vn[w] = seed;
         if (w < p.words) p.B2[w] = (w == src_word) ? src_bit : 0u;  // α of the source's set, level 1
+    }
+    if (gtid == 0) {  // sentinel word after the visited bitmaps: "visited" for every bit
+        Vc[vwords] = ~0u;
+        Vn[vwords] = ~0u;
     }
     if (threadIdx.x == 0) {
         p.agg[blockIdx.x] = 0;
@@ -197,20 +189,37 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         };
         const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
         const uint32_t* W = recheck ? Vc : Vn;
-        // loads of the VSSs named by lanes 0..kBatchLazy-1 of e, then their visited tests
+        // Loads of the VSSs named by lanes 0..kBatchLazy-1 of e, then their visited tests.
+        // An absent batch slot carries entry 0 (VSS 0 with α = 0): its loads are harmless
+        // and its pull finds no candidate, so no per-slot predication is needed.
+        const uint32_t sent = (uint32_t)vwords;  // sentinel word (all ones) after the bitmap
         auto pull_batch = [&](unsigned long long e) {
-            uint32_t mk[kBatchLazy];
+            uint32_t mk[kBatchLazy], a[kBatchLazy];
             uint4 rw[kBatchLazy];
 #pragma unroll
             for (int j = 0; j < kBatchLazy; ++j) {
-                const unsigned long long ej = __shfl_sync(0xffffffffu, e, j);
-                const bool ok = ej != kNoEntry;
-                const uint64_t v = ok ? (uint32_t)ej : 0u;
-                mk[j] = ok ? ld_stream_u32(p.masks + 32 * v + lane, pol) : 0u;
-                rw[j] = ok ? ld_stream_u4(rows4 + 32 * v + lane, pol) : make_uint4(0, 0, 0, 0);
+                const uint32_t v = __shfl_sync(0xffffffffu, (uint32_t)e, j);
+                a[j] = __shfl_sync(0xffffffffu, (uint32_t)(e >> 32), j);  // α (0 when absent)
+                mk[j] = ld_stream_u32(p.masks + 32 * (uint64_t)v + lane, pol);
+                rw[j] = ld_stream_u4(rows4 + 32 * (uint64_t)v + lane, pol);
             }
-            ctr[2] += check_batch<PULL>(p, W, Vn, recheck, e, [&](int j) { return rw[j]; },
-                                        [&](int j) { return mk[j]; });
+            if (PULL == 0) {
+                uint32_t x[kBatchLazy];  // mask & α in every column byte
+#pragma unroll
+                for (int j = 0; j < kBatchLazy; ++j) x[j] = mk[j] & (a[j] * 0x01010101u);
+                ctr[2] += check_batch(W, Vn, recheck, sent, rw,
+                                      [&](int j, int c) { return (x[j] & (0xFFu << (8 * c))) != 0u; });
+            } else {
+                uint32_t cm[kBatchLazy];  // column hits from the b1 tile (bit c = column c)
+#pragma unroll
+                for (int j = 0; j < kBatchLazy; ++j) {
+                    uint32_t cnt[4];
+                    column_counts<PULL>(mk[j], a[j], cnt);
+                    cm[j] = (cnt[0] != 0) | ((cnt[1] != 0) << 1) | ((cnt[2] != 0) << 2) | ((cnt[3] != 0) << 3);
+                }
+                ctr[2] += check_batch(W, Vn, recheck, sent, rw,
+                                      [&](int j, int c) { return ((cm[j] >> c) & 1u) != 0u; });
+            }
         };
         if (len < p.dense_min) {
             // ---- sparse level: every warp expands its own contiguous share of the queue
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
                         const uint32_t cnt = (hi - c0 < 32) ? (uint32_t)(hi - c0) : 32u;
                         for (uint32_t k = 0; k < cnt; k += kBatchLazy) {
                             unsigned long long e = __shfl_sync(0xffffffffu, mine, (lane + k) & 31);
-                            if (lane >= (uint32_t)kBatchLazy || k + lane >= cnt) e = kNoEntry;
+                            if (lane >= (uint32_t)kBatchLazy || k + lane >= cnt) e = 0;  // absent
                             pull_batch(e);
                         }
                     }
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
                     const uint64_t step = qs * kBatchLazy;
                     auto qload = [&](uint64_t base) -> unsigned long long {
                         const uint64_t pos = base + (uint64_t)lane * qs;
-                        return (lane < kBatchLazy && pos < qe) ? Qc[pos] : kNoEntry;
+                        return (lane < kBatchLazy && pos < qe) ? Qc[pos] : 0ull;  // 0: absent
                     };
                     unsigned long long e_next = qload(q0);
                     for (uint64_t p0 = q0; p0 < qe; p0 += step) {

@@ -100,6 +100,17 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p, uint64_t pol) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
     return v;
 }
+// Predicated streaming row-id load: lanes whose pull found no candidate (every column's
+// mask & α is 0) skip it and get zeros — pull_vss never dereferences their row ids
+// (R:src/bfs_engine.cpp:131-146), so a 128 B line none of its 8 lanes needs is not fetched.
+__device__ __forceinline__ uint4 ld_stream_u4_if(bool pred, const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+        "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "r"((uint32_t)pred), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

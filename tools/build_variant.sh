@@ -1,14 +1,15 @@
 #!/bin/bash
 # Build an experiment variant of the library: tools/build_variant.sh NAME "-DFLAG=..." [SRC_DIR]
-# -> build/exp/NAME/libblest_b200.so (select at run time with BLEST_LIB=...).
+# -> variants/NAME/libblest_b200.so (select at run time with BLEST_LIB=...; travels to the GPU box).
 set -e
 NAME=$1; FLAGS=$2; SRC=${3:-paper_2512_21967_b200/csrc}
-OUT=build/exp/$NAME; mkdir -p $OUT
+OUT=variants/$NAME; OBJ=$(mktemp -d); mkdir -p $OUT
 for f in $SRC/*.cu; do
   b=$(basename $f .cu)
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-     --expt-relaxed-constexpr -Iinclude $FLAGS -c $f -o $OUT/$b.o &
+     --expt-relaxed-constexpr -Iinclude $FLAGS -c $f -o $OBJ/$b.o &
 done
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libblest_b200.so $OUT/*.o -lcudart
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libblest_b200.so $OBJ/*.o -lcudart
+rm -rf $OBJ
 echo $OUT/libblest_b200.so
