@@ -200,8 +200,9 @@ def engine_policy_lazy(n: int, m: int, num_vss: int) -> bool:
     return m >= 8 * max(n, 1) and num_vss >= (1 << 20)
 
 
-def prepare(config: str, ordering_override: str | None, window: int):
-    """Generate -> (relabel) -> plan/order -> permute -> build, all on the GPU."""
+def prepare(config: str, ordering_override: str | None, window: int, build: bool = True):
+    """Generate -> (relabel) -> plan/order -> permute -> build, all on the GPU (build=False:
+    the row-partitioned mode builds one BVSS slice per rank instead)."""
     import paper_2512_21967_b200 as B
     kind, prm, ordering, desc = CONFIGS[config]
     ordering = ordering_override or ordering
@@ -224,9 +225,11 @@ def prepare(config: str, ordering_override: str | None, window: int):
     t_order = time.time() - t0
     t0 = time.time()
     gp = g if perm.is_identity() else B.apply_permutation(g, perm)
-    b = B.build_bvss(gp)
-    b.producing_permutation = perm
-    b.ordering_tag = plan.strategy.value
+    b = None
+    if build:
+        b = B.build_bvss(gp)
+        b.producing_permutation = perm
+        b.ordering_tag = plan.strategy.value
     t_build = time.time() - t0
     return dict(g=g, gp=gp, b=b, plan=plan, perm=perm, desc=desc, ordering=ordering,
                 times=dict(generate_s=round(t_gen, 3), order_s=round(t_order, 3), build_s=round(t_build, 3)))
@@ -395,10 +398,15 @@ def main():
     ap.add_argument("--validate", type=int, default=-1,
                     help="parity: check this many timed sources against the CPU reference BFS on a host-built "
                          "original graph (-1 = all, 0 = off)")
-    ap.add_argument("--partition", default="replicas", choices=["replicas", "rows"],
-                    help="N>1: source-sharded replicas (default) or one BFS row-partitioned over the ranks")
+    ap.add_argument("--partition", default=None, choices=["replicas", "rows"],
+                    help="N>1: rows (default: one BFS row-partitioned over the ranks, SURVEY 8(e)) or "
+                         "replicas (every rank holds the whole structure and runs its share of the sources)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="rows mode: nccl = one launch per level + ncclAllGather of the frontier words; "
+                         "p2p = one launch per BFS, frontier words stored into the peers' buffers over "
+                         "CUDA IPC (NVLink) with an in-kernel cross-rank barrier")
     ap.add_argument("--virtual-ranks", type=int, default=0,
-                    help="rows partition emulated on one GPU with this many ranks (lock-step, device concat)")
+                    help="rows partition emulated on one GPU with this many ranks (p2p exchange in one launch)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -431,8 +439,16 @@ def main():
     stream = torch.cuda.current_stream()
     L.check(lib.blest_set_stream(C.c_void_p(stream.cuda_stream)))
 
-    prep = prepare(args.config, args.order, args.window)
+    if args.partition is None:
+        args.partition = "rows" if world > 1 else "replicas"
+    rows_mode = args.partition == "rows" or args.virtual_ranks > 0
+    prep = prepare(args.config, args.order, args.window, build=not rows_mode)
     g, b, plan, perm = prep["g"], prep["b"], prep["plan"], prep["perm"]
+    if rows_mode:
+        run_partitioned(args, prep, B, L, lib, perm, world, rank, local, stream)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.mode == "b200":
         # measured: lazy wins on large Kron and urand (C3 2.7 vs 4.75 ms), eager on grids (many
         # levels) and on small graphs, where lazy's ~15 µs fixed stage-2 cost per level
@@ -456,10 +472,6 @@ def main():
                         if b.num_vss * 644 >= 2 * 126e6 else
                         "BVSS %.1f MB fits in L2: 512 MB L2 flush before every timed BFS" % (b.num_vss * 644 / 1e6)),
                     prep_s=prep["times"], parallelism=f"source-sharded x{world}" if world > 1 else "1 GPU")
-
-    if args.partition == "rows" or args.virtual_ranks:
-        run_partitioned(args, prep, B, L, lib, srcs_orig, perm, world, rank, local, workload, stream)
-        return
 
     ecfg = L.EngineConfigT(L.MODE_LAZY if lazy else L.MODE_EAGER,
                            L.PULL_MMA if args.pull == "mma" else L.PULL_POPC, 0, 0, args.grid_ctas, args.threads)
@@ -618,71 +630,188 @@ def main():
         dist.destroy_process_group()
 
 
-def run_partitioned(args, prep, B, L, lib, srcs_orig, perm, world, rank, local, workload, stream):
-    """Row-partitioned BFS: every rank owns a 32-aligned range of destination
-    rows and its BVSS slice; per level a NCCL all-gather of the frontier diff words. Each
-    step = one BFS from the next source over all ranks; value = harmonic-mean GTEPS of that
-    distributed BFS (whole job), timed on each rank's device, max over ranks."""
+def run_partitioned(args, prep, B, L, lib, perm, world, rank, local, stream):
+    """Row-partitioned BFS (csrc/rows.cu): rank g owns a slice-balanced range
+    of destination rows and the BVSS of A[rows_g, all columns], built on its own GPU. Each
+    step = one BFS from the next source over all ranks (strong scaling); value = harmonic-
+    mean GTEPS of the distributed BFS, each BFS timed with CUDA events on every rank's
+    stream, max over ranks. --exchange nccl: one launch per level + ncclAllGather of the
+    n/8-byte frontier (host never waits on a level); p2p: one launch per BFS, peer stores
+    over CUDA IPC; --virtual-ranks G: G ranks of this GPU in one launch (p2p protocol)."""
     import torch
     import torch.distributed as dist
-    from paper_2512_21967_b200.multigpu import (GpuPartition, RowPartitionedBfs, nccl_allgather, partition_rows,
-                                                 run_lockstep, words_per_rank)
+    from paper_2512_21967_b200 import multigpu as MG
     gp = prep["gp"]
     n = gp.num_vertices()
     deg = gp.out_degrees().astype(np.int64)
+    total = args.steps * 1 + args.warmup
+    srcs_orig = gp.pick_sources(total, args.source_seed) if perm.is_identity() else \
+        prep["g"].pick_sources(total, args.source_seed)
     srcs = perm.forward_map()[srcs_orig] if not perm.is_identity() else srcs_orig
-    steps = srcs[args.warmup: args.warmup + args.steps]
-    if args.virtual_ranks:
-        G = args.virtual_ranks
-        per = words_per_rank(n, G)
-        parts = [GpuPartition(gp, lo, hi, per) for lo, hi in partition_rows(n, G)]
-        run = lambda s: run_lockstep(parts, n, int(s))[0]
-        mode = f"rows x{G} virtual ranks on 1 GPU"
+    warm, steps = srcs[: args.warmup], srcs[args.warmup: args.warmup + args.steps]
+    virtual = args.virtual_ranks > 0
+    G = args.virtual_ranks if virtual else world
+    t0 = time.time()
+    bounds, slices = MG.partition_rows(gp, G)
+    t_part = time.time() - t0
+    t0 = time.time()
+    if virtual:
+        engs = [MG.RowsEngine(gp, r, G, bounds) for r in range(G)]
+        MG.set_local_peers(engs)
+        mode = f"rows x{G} virtual ranks on 1 GPU (p2p exchange protocol, one launch per BFS)"
+
+        def run(s):
+            MG.group_bfs(engs, int(s))
+
+        def results(levels):
+            return [e.finish(levels) for e in engs]
     else:
-        G = world
-        lo, hi = partition_rows(n, G)[rank]
-        part = GpuPartition(gp, lo, hi, words_per_rank(n, G))
-        bfs = RowPartitionedBfs(part, n, nccl_allgather())
-        run = lambda s: bfs.run(int(s))
-        mode = f"rows x{G} ranks, {dist.get_backend().upper()} all-gather per level"
-    del prep["b"]  # the single-GPU structure is not used by this mode
-    for s in srcs[: args.warmup]:
-        run(s)
-    times, edges = [], []
-    for s in steps:
+        eng = MG.RowsEngine(gp, rank, G, bounds)
+        engs = [eng]
+        if args.exchange == "p2p":
+            MG.exchange_ipc_handles(eng)
+            mode = f"rows x{G} ranks, p2p: frontier words stored into peers over CUDA IPC, one launch per BFS"
+
+            def run(s):
+                eng.bfs(int(s))
+        else:
+            stepper = MG.SteppedBfs(eng, MG.torch_allgather(), ahead=2)
+            mode = f"rows x{G} ranks, {dist.get_backend().upper()} all-gather of the frontier per level"
+
+            def run(s):
+                stepper.run(int(s), levels=False)
+
+        def results(levels):
+            return [eng.finish(levels)]
+    torch.cuda.synchronize()
+    t_build = time.time() - t0
+    arcs = int(gp.num_edges())
+    del prep["gp"]
+    vss = [e.num_vss for e in engs]
+    if not virtual and world > 1:
+        tv = torch.tensor([float(v) for v in vss], dtype=torch.float64, device=coll_dev())
+        allv = [torch.zeros_like(tv) for _ in range(world)]
+        dist.all_gather(allv, tv)
+        vss = [int(x.item()) for x in allv]
+
+    def sync_all():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    for s in warm:
+        run(s)
+        results(False)
+    clk = ClockSampler(local).start()
+    launches0 = lib.blest_kernel_launches()
+    times, edges, queues, iters = [], [], [], []
+    for s in steps:
+        sync_all()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if rank == 0:
+            clk.mark()
         e0.record(stream)
-        r = run(s)
+        run(s)
         e1.record(stream)
         torch.cuda.synchronize()
+        if rank == 0:
+            clk.unmark()
+        res = results(True)
         t = e0.elapsed_time(e1) / 1e3
-        if args.virtual_ranks:
-            reached = r != 0xFFFFFFFF
-            e = int(deg[reached].sum()) // 2
-        else:
-            reached = r.levels != 0xFFFFFFFF
-            e = int(deg[r.row_lo:r.row_hi][reached].sum())
-        if world > 1 and not args.virtual_ranks:
-            tt = torch.tensor([t, float(e)], dtype=torch.float64, device=coll_dev())
+        e = sum(int(deg[r.row_lo:r.row_hi][r.levels != 0xFFFFFFFF].sum()) for r in res)
+        q = sum(r.queue for r in res)
+        if world > 1 and not virtual:
+            tt = torch.tensor([t, float(e), float(q)], dtype=torch.float64, device=coll_dev())
             tmax = tt.clone()
-            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-            t, e = float(tmax[0].item()), int(tt[1].item()) // 2
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            t, e, q = float(tmax[0].item()), int(tt[1].item()), int(tt[2].item())
         times.append(t)
-        edges.append(e)
+        edges.append(e // 2)
+        queues.append(q)
+        iters.append(res[0].iterations)
+    clk.stop()
+    launches = lib.blest_kernel_launches() - launches0
     t = np.array(times)
     E = np.array(edges, np.float64)
     hm = len(t) / float(np.sum(t / E)) / 1e9
+
+    # ---- e2e: the public call per BFS with the owned levels copied to host, wall clock ----
+    te = []
+    for s in steps[: min(8, len(steps))]:
+        sync_all()
+        w0 = time.perf_counter()
+        run(s)
+        results(True)
+        w = time.perf_counter() - w0
+        if world > 1 and not virtual:
+            tw = torch.tensor([w], dtype=torch.float64, device=coll_dev())
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+            w = float(tw.item())
+        te.append(w)
+    te = np.array(te)
+    e2e_hm = len(te) / float(np.sum(te / E[: len(te)])) / 1e9
+
+    # ---- parity: assembled levels of the first timed sources vs the CPU reference BFS ----
+    parity = None
+    nval = len(steps) if args.validate < 0 else min(args.validate, len(steps))
+    nval = min(nval, 8)
+    if nval:
+        gathered = []
+        for s in steps[:nval]:
+            run(s)
+            res = results(True)
+            if virtual:
+                gathered.append(MG.assemble(res, n))
+            else:
+                r = res[0]
+                per_rows = 32 * max(b - a for a, b in zip(bounds, bounds[1:]))
+                mine = torch.full((per_rows,), -1, dtype=torch.int64, device=coll_dev())
+                mine[: r.row_hi - r.row_lo] = torch.from_numpy(r.levels.astype(np.int64)).to(coll_dev())
+                parts = [torch.empty_like(mine) for _ in range(world)]
+                dist.all_gather(parts, mine)
+                if rank == 0:
+                    full = np.concatenate([p.cpu().numpy()[: min(32 * bounds[i + 1], n) - min(32 * bounds[i], n)]
+                                           for i, p in enumerate(parts)])
+                    gathered.append(full.astype(np.uint32))
+        if rank == 0:
+            fm = None if perm.is_identity() else perm.forward_map()
+            parity, gcpu = validate_levels(args.config, os.cpu_count() or 1, srcs_orig[args.warmup: args.warmup + nval],
+                                           gathered, fm, edges[:nval])
+            del gcpu
+            log(f"parity (rows x{G}): {parity['checked']} sources, {parity['mismatches']} mismatches")
     if rank == 0:
-        workload = dict(workload, parallelism=mode)
-        print(json.dumps(dict(metric="GTEPS (harmonic mean over sources)", value=round(hm, 4), unit="GTEPS",
-                              n_gpus=world, steps=len(t), warmup=args.warmup,
-                              ms_per_step=round(1e3 * float(t.mean()), 4), higher_is_better=True,
-                              scaling="strong", vs_baseline=None, dtype="u32", data="synthetic",
-                              config=workload, detail=dict(mean_traversed_edges=int(E.mean())))), flush=True)
+        peak, peak_kind = load_peaks()
+        stream_b = 648.0 * float(np.mean(queues))
+        achieved = stream_b / float(t.mean()) / 1e9 / G
+        workload = dict(workload=args.config, graph=prep["desc"], n=n, arcs=arcs,
+                        ordering=prep["plan"].strategy.value, engine="lazy (row-partitioned)",
+                        partition=dict(ranks=G, word_bounds=[int(x) for x in bounds], slices=[int(x) for x in slices],
+                                       vss=vss, balance="BVSS slice count (blest_partition_rows)"),
+                        exchange="p2p" if (virtual or args.exchange == "p2p") else "nccl",
+                        sources=len(steps), source_seed=args.source_seed,
+                        prep_s=dict(prep["times"], partition_s=round(t_part, 3), rank_build_s=round(t_build, 3)),
+                        parallelism=mode,
+                        l2="inputs larger than L2 (BVSS slices >> 126 MB), no flush" if sum(vss) * 644 > 2 * 126e6
+                        else "structure fits in L2 (no flush in rows mode)")
+        line = dict(metric="GTEPS (harmonic mean over sources)", value=round(hm, 4), unit="GTEPS", n_gpus=world,
+                    steps=len(t), warmup=len(warm), ms_per_step=round(1e3 * float(t.mean()), 4),
+                    higher_is_better=True, scaling="strong", vs_baseline=None, dtype="u32", data="synthetic",
+                    config=workload,
+                    roofline=dict(bound="hbm", achieved=round(achieved, 1), peak=peak, unit="GB/s",
+                                  frac=round(achieved / peak, 4), traffic=None,
+                                  peak_source=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs), per GPU",
+                                  formula="648 B x (sum over ranks of the local VSS queue) / time / GPUs: the "
+                                          "stage-1 BVSS stream per GPU"),
+                    e2e=dict(value=round(e2e_hm, 4), unit="GTEPS", h2d_bytes_per_step=4,
+                             d2h_bytes_per_step=int(4 * n),
+                             note="the public call per BFS (launches + exchange) and every rank's owned levels "
+                                  "copied to host, wall clock, max over ranks"),
+                    gpu_launches=int(launches), parity=parity, clocks=clk.summary(),
+                    detail=dict(mean_levels=float(np.mean(iters)), mean_traversed_edges=int(E.mean()),
+                                mean_local_queue_sum=int(np.mean(queues)),
+                                min_ms=round(1e3 * float(t.min()), 4), max_ms=round(1e3 * float(t.max()), 4)))
+        print(json.dumps(line), flush=True)
 
 
 def census_of(lib, L, b, prep, sources, lazy, pull, threads=0, grid_ctas=0, keep_levels=()):

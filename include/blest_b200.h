@@ -231,24 +231,55 @@ int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads);
  * build_fragB(alpha)). For the reference's tile KATs (R:tests/tc_emu_test.cpp:186-241). */
 int blest_tile_pull(const uint32_t* masks, const uint8_t* alpha, uint32_t count, uint32_t* counts);
 
-/* ---- row-partitioned multi-GPU mode (no reference counterpart) ---------- */
+/* ---- row-partitioned multi-GPU mode (no reference counterpart: the paper
+ * lists multi-GPU as future work) -------------------------------------------
+ * Rank g of `world` owns destination rows [32*word_bounds[g], 32*word_bounds[g+1]) and a
+ * BVSS of A[those rows, all columns] (row ids stay global). Per level: lazy stage 1 over
+ * the local VSSs, the owned V words swept (levels, diff), the n/8-byte frontier exchanged
+ * (each word has one writer, so no OR-reduction), the whole frontier swept by every rank
+ * (termination, next queue). Two exchange modes, one kernel:
+ *   fused   — blest_rows_bfs: one cooperative launch per BFS per rank; diff words stored
+ *             into every peer's frontier buffer over CUDA IPC (NVLink), cross-rank
+ *             arrival barrier in the kernel; blest_rows_group_bfs runs G virtual ranks of
+ *             one device in one launch;
+ *   stepped — blest_rows_step: one launch per level; the caller all-gathers every rank's
+ *             send buffer (ncclAllGather / torch.distributed) on the same stream into recv.
+ * Everything is ordered on the library stream; nothing here synchronises the host. */
+typedef struct blest_rows_s* blest_rows;
+typedef struct {
+    uint32_t iterations;  /* level iterations (including the final barren one) */
+    uint32_t max_level;   /* deepest level with a discovery in the owned rows */
+    uint64_t queue;       /* sum over levels of the local VSS queue */
+    uint64_t discovered;  /* owned rows discovered (source excluded) */
+    uint64_t relaxed;     /* stage-1 REDs issued */
+    uint64_t pushes;      /* local VSSs queued for next levels */
+} blest_rows_stats;
+/* Row ranges balanced by BVSS slice count (one slice = a (column slice set, row) pair, the
+ * unit of pull work): word_bounds[0..world], slices[0..world-1] (optional) per rank. */
+int blest_partition_rows(blest_graph g, uint32_t world, uint64_t* word_bounds, uint64_t* slices);
 /* BVSS of A[rows [row_lo, row_hi), all columns] (row_lo 32-aligned, row_hi 32-aligned or n):
- * every column slice set keeps its VSS range, row ids stay global. One rank = one range. */
+ * every column slice set keeps its VSS range, row ids stay global (one rank's slice). */
 int blest_bvss_build_rows(blest_graph g, uint32_t row_lo, uint32_t row_hi, blest_bvss* out);
-/* Owned rows and owned frontier words [word_lo, word_hi). */
-int blest_part_range(blest_bvss b, uint32_t* row_lo, uint32_t* row_hi, uint64_t* word_lo, uint64_t* word_hi);
-/* init_state for this rank (R:src/bfs_engine.cpp:30-49 restricted to owned rows). */
-int blest_part_begin(blest_bvss b, uint32_t src, uint64_t* queue_len);
-/* Stage 1 of one level over the local queue (lazy pull, R:src/bfs_engine.cpp:273-292). */
-int blest_part_pull(blest_bvss b);
-/* Stage 2 over the owned words (R:src/bfs_engine.cpp:296-338): levels written, the owned
- * diff words stored to diff_out (device, word_hi-word_lo words) for the all-gather. */
-int blest_part_sweep(blest_bvss b, uint32_t level, uint32_t* diff_out, uint64_t* discovered);
-/* After the all-gather: queue this rank's VSSs of every active set of the full diff
- * (device, ceil(n/32) words); total_discovered = set bits over all ranks (0 = done). */
-int blest_part_enqueue(blest_bvss b, const uint32_t* full_diff, uint64_t* queue_len, uint64_t* total_discovered);
-/* Levels of the owned rows (host, row_hi-row_lo entries). */
-int blest_part_levels(blest_bvss b, uint32_t* levels_out);
+/* This rank's engine: builds its BVSS slice from g (device) with the given bounds. */
+int blest_rows_create(blest_graph g, uint32_t rank, uint32_t world, const uint64_t* word_bounds, blest_rows* out);
+int blest_rows_info(blest_rows r, uint32_t* row_lo, uint32_t* row_hi, uint32_t* num_vss, uint64_t* per_words);
+/* fused mode plumbing: this rank's IPC handle (64 bytes); every rank's (world x 64 bytes,
+ * rank-major) to map the peers; or the sibling engines of one device (virtual ranks). */
+int blest_rows_ipc_handle(blest_rows r, void* handle64);
+int blest_rows_open_peers(blest_rows r, const void* handles);
+int blest_rows_set_local_peers(blest_rows* ranks, uint32_t world);
+int blest_rows_bfs(blest_rows r, uint32_t src);
+int blest_rows_group_bfs(blest_rows* ranks, uint32_t world, uint32_t src);
+/* stepped mode: level 1 starts a BFS from src; level > 1 reads recv (device, world x
+ * per_words u32, rank-major: the all-gather of every rank's send buffer). send: device,
+ * per_words u32 (the rank's owned diff words, zero-padded). flags (mapped host memory,
+ * no sync): progress = last level launched, done = iterations once finished (else 0). */
+int blest_rows_step(blest_rows r, uint32_t level, uint32_t src, const uint32_t* recv);
+int blest_rows_send_buffer(blest_rows r, uint32_t** send);
+int blest_rows_flags(blest_rows r, uint32_t* progress, uint32_t* done, uint32_t* status);
+/* Waits for the stream; owned rows' levels (host, row_hi-row_lo entries; may be NULL). */
+int blest_rows_finish(blest_rows r, uint32_t* levels_owned, blest_rows_stats* out);
+int blest_rows_free(blest_rows r);
 
 #ifdef __cplusplus
 }

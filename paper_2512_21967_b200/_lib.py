@@ -96,6 +96,11 @@ class LevelTraceT(C.Structure):
                 ("relaxed_atomics", C.c_uint64), ("queue_pushes", C.c_uint64)]
 
 
+class RowsStatsT(C.Structure):
+    _fields_ = [("iterations", C.c_uint32), ("max_level", C.c_uint32), ("queue", C.c_uint64),
+                ("discovered", C.c_uint64), ("relaxed", C.c_uint64), ("pushes", C.c_uint64)]
+
+
 # Every symbol include/blest_b200.h declares, with its ctypes signature.
 vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
 P = C.POINTER
@@ -148,12 +153,19 @@ SIGNATURES = {
     "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),
     "blest_bvss_build_rows": (i32, [vp, u32, u32, P(vp)]),
-    "blest_part_range": (i32, [vp, P(u32), P(u32), P(u64), P(u64)]),
-    "blest_part_begin": (i32, [vp, u32, P(u64)]),
-    "blest_part_pull": (i32, [vp]),
-    "blest_part_sweep": (i32, [vp, u32, vp, P(u64)]),
-    "blest_part_enqueue": (i32, [vp, vp, P(u64), P(u64)]),
-    "blest_part_levels": (i32, [vp, vp]),
+    "blest_partition_rows": (i32, [vp, u32, vp, vp]),
+    "blest_rows_create": (i32, [vp, u32, u32, vp, P(vp)]),
+    "blest_rows_info": (i32, [vp, P(u32), P(u32), P(u32), P(u64)]),
+    "blest_rows_ipc_handle": (i32, [vp, vp]),
+    "blest_rows_open_peers": (i32, [vp, vp]),
+    "blest_rows_set_local_peers": (i32, [vp, u32]),
+    "blest_rows_bfs": (i32, [vp, u32]),
+    "blest_rows_group_bfs": (i32, [vp, u32, u32]),
+    "blest_rows_step": (i32, [vp, u32, u32, vp]),
+    "blest_rows_send_buffer": (i32, [vp, P(vp)]),
+    "blest_rows_flags": (i32, [vp, P(u32), P(u32), P(u32)]),
+    "blest_rows_finish": (i32, [vp, vp, P(RowsStatsT)]),
+    "blest_rows_free": (i32, [vp]),
 }
 
 _lib = None

@@ -317,54 +317,6 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
 }
 
 
-// One warp's view of 32 consecutive SL entries.
-struct SetWindow {
-    uint32_t base;   // SL index held by lane 0
-    uint64_t first;  // lane's first queue position (UINT64_MAX past the list)
-    uint32_t b;      // lane's first VSS id (real_ptrs[s])
-    uint32_t alpha;  // lane's frontier byte
-    uint64_t wend;   // one past the last position covered by the window
-};
-
-__device__ __forceinline__ void load_window(const Params& p, const uint8_t* Fd8, uint32_t base, uint32_t S,
-                                            uint64_t T, SetWindow& w) {
-    const unsigned lane = lane_id();
-    const uint32_t k = base + lane;
-    uint64_t first = ~0ull, nxt = T;
-    uint32_t b = 0, alpha = 0;
-    if (k < S) {
-        const unsigned long long e = p.SL[k];
-        first = e >> 32;
-        const uint32_t ss = (uint32_t)e;
-        b = p.rp[ss];
-        alpha = Fd8[ss];
-        if (lane == 31 && k + 1 < S) nxt = p.SL[k + 1] >> 32;
-    }
-    w.base = base;
-    w.first = first;
-    w.b = b;
-    w.alpha = alpha;
-    w.wend = (base + 32 < S) ? __shfl_sync(0xffffffffu, nxt, 31) : T;
-}
-
-// Largest SL index k with first(k) <= pos (first(0) = 0, entries ascending).
-__device__ __forceinline__ uint32_t find_set(const Params& p, uint32_t S, uint64_t pos) {
-    const unsigned lane = lane_id();
-    uint32_t lo = 0, hi = S;
-    while (hi - lo > 32) {
-        const uint32_t step = (hi - lo + 31) / 32;
-        const uint32_t idx = lo + lane * step;
-        const bool ok = idx < hi && (p.SL[idx] >> 32) <= pos;
-        const unsigned ball = __ballot_sync(0xffffffffu, ok);
-        lo = lo + (31 - __clz(ball)) * step;
-        hi = min(hi, lo + step);
-    }
-    const uint32_t idx = lo + lane;
-    const bool ok = idx < hi && (p.SL[idx] >> 32) <= pos;
-    return lo + (31 - __clz(__ballot_sync(0xffffffffu, ok)));
-}
-
-
 // Lazy stage 2 (R:src/bfs_engine.cpp:296-338), shared by both lazy kernels. The ⌈n/32⌉
 // words are cut into chunks of 4·THREADS (one uint4 of words per thread) and each CTA owns
 // a contiguous run of chunks. Pass A, per chunk: diff = V_next & ~V_curr, V_curr = V_next,

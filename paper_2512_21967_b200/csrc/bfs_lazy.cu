@@ -22,6 +22,7 @@
 // and B3 by level parity, so the next level's can be cleared while this one is read.
 #include "bfs.cuh"
 #include "bfs_device.cuh"
+#include "lazy_pull.cuh"
 
 namespace blestgpu {
 
@@ -32,60 +33,6 @@ using namespace bfsdev;
 #ifndef BLEST_MINB
 #define BLEST_MINB 1
 #endif
-// Visited tests of one batch (kBatchLazy VSSs × 4 columns per lane) in batch-wide phases,
-// each phase's memory operations in flight together (one latency per phase, not one per
-// VSS): (A) every (VSS, column) slot's word of the test bitmap W — the row's word when the
-// lane's pull hit the column, else the sentinel word `sent` (all ones, L1-resident), so the
-// load is unconditional and needs no default move; (B) optionally (Params::recheck) the
-// words still clear re-read from V_next at L2; (C) a fire-and-forget RED into V_next for
-// every bit still clear (legal per SURVEY §8(a) pitfall 7). Default W = V_next without (B):
-// V_next ⊇ V_curr, so a set bit means "visited before, or already marked this level", and
-// an L1 copy lagging this level's REDs from other SMs only costs an extra idempotent RED
-// (the grid barrier invalidates L1 between levels). W = V_curr with (B) is the older
-// scheme (V_curr is frozen within the level; the L2 re-check spares REDs). hit[j] holds
-// the lane's 4 column hits of VSS j in bits 0..3; rw[j] its row ids. Returns the REDs
-// issued. The stage is instruction-issue bound as much as latency bound (C2 level 3:
-// ~124 warp instructions per VSS at ~74 % of the SM issue rate), so every phase is a
-// straight line of LOP3 / SHF / SEL / IMAD.WIDE / LDG|RED per slot.
-// (Codegen note: the optional phase B branch also keeps ptxas from interleaving phase
-// A's result moves with its later loads — without it the same default path measured
-// 5.3 ms per BFS.)
-template <typename Hit>
-__device__ __forceinline__ uint32_t check_batch(const uint32_t* W, uint32_t* Vn, bool recheck, uint32_t sent,
-                                                const uint4 (&rw)[kBatchLazy], Hit hit) {
-    uint32_t vw[4 * kBatchLazy];
-#pragma unroll
-    for (int j = 0; j < kBatchLazy; ++j) {
-        const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) vw[4 * j + c] = W[hit(j, c) ? (u[c] >> 5) : sent];
-    }
-    if (recheck) {
-#pragma unroll
-        for (int j = 0; j < kBatchLazy; ++j) {
-            const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) vw[4 * j + c] = recheck_word(Vn, u[c], vw[4 * j + c]);
-        }
-    }
-    uint32_t reds = 0;
-#pragma unroll
-    for (int j = 0; j < kBatchLazy; ++j) {
-        const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            // ptxas never predicates a global RED (it branches around it), so the count
-            // lives inside the same branch: executed only when some lane issues the RED
-            const uint32_t bit = __funnelshift_l(0u, 1u, u[c]);
-            if (!(vw[4 * j + c] & bit)) {
-                red_or(Vn + (u[c] >> 5), bit);
-                ++reds;
-            }
-        }
-    }
-    return reds;
-}
-
 template <int PULL, int THREADS, bool SIGMA>
 #ifndef BLEST_LAZY_MINB
 #define BLEST_LAZY_MINB (BLEST_MINB > 1 ? BLEST_MINB : 1024 / THREADS)
@@ -168,132 +115,37 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         const uint32_t* Fd = (level & 1) ? p.B2 : p.B3;
         uint32_t* Fn = (level & 1) ? p.B3 : p.B2;
         const uint8_t* Fd8 = reinterpret_cast<const uint8_t*>(Fd);
-        // queue entry (α << 32 | VSS) of position c0 + lane; `win` is slid forward as needed
-        auto entry_at = [&](uint64_t c0, SetWindow& win) -> unsigned long long {
-            if (c0 + 31 >= win.wend && win.wend < len) {  // slide to the set holding c0
-                const unsigned own = __ballot_sync(0xffffffffu, win.first <= c0);
-                const uint32_t nb = (c0 >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
-                load_window(p, Fd8, nb, S, len, win);
-            }
-            const uint64_t q = c0 + lane;
-            int l = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint64_t f = __shfl_sync(0xffffffffu, win.first, l + step);
-                if (f <= q) l += step;
-            }
-            const uint32_t v = __shfl_sync(0xffffffffu, win.b, l) +
-                               (uint32_t)(q - __shfl_sync(0xffffffffu, win.first, l));
-            const uint32_t a = __shfl_sync(0xffffffffu, win.alpha, l);
-            return ((unsigned long long)a << 32) | v;
-        };
         const bool recheck = p.lazy_recheck != 0;  // W = V_curr + V_next re-check (older scheme)
-        const uint32_t* W = recheck ? Vc : Vn;
-        // Loads of the VSSs named by lanes 0..kBatchLazy-1 of e, then their visited tests.
-        // An absent batch slot carries entry 0 (VSS 0 with α = 0): its loads are harmless
-        // and its pull finds no candidate, so no per-slot predication is needed.
-        const uint32_t sent = (uint32_t)vwords;  // sentinel word (all ones) after the bitmap
-        auto pull_batch = [&](unsigned long long e) {
-            uint32_t mk[kBatchLazy], a[kBatchLazy];
-            uint4 rw[kBatchLazy];
-#pragma unroll
-            for (int j = 0; j < kBatchLazy; ++j) {
-                const uint32_t v = __shfl_sync(0xffffffffu, (uint32_t)e, j);
-                a[j] = __shfl_sync(0xffffffffu, (uint32_t)(e >> 32), j);  // α (0 when absent)
-                mk[j] = ld_stream_u32(p.masks + 32 * (uint64_t)v + lane, pol);
-                rw[j] = ld_stream_u4(rows4 + 32 * (uint64_t)v + lane, pol);
-            }
-            if (PULL == 0) {
-                uint32_t x[kBatchLazy];  // mask & α in every column byte
-#pragma unroll
-                for (int j = 0; j < kBatchLazy; ++j) x[j] = mk[j] & (a[j] * 0x01010101u);
-                ctr[2] += check_batch(W, Vn, recheck, sent, rw,
-                                      [&](int j, int c) { return (x[j] & (0xFFu << (8 * c))) != 0u; });
-            } else {
-                uint32_t cm[kBatchLazy];  // column hits from the b1 tile (bit c = column c)
-#pragma unroll
-                for (int j = 0; j < kBatchLazy; ++j) {
-                    uint32_t cnt[4];
-                    column_counts<PULL>(mk[j], a[j], cnt);
-                    cm[j] = (cnt[0] != 0) | ((cnt[1] != 0) << 1) | ((cnt[2] != 0) << 2) | ((cnt[3] != 0) << 3);
-                }
-                ctr[2] += check_batch(W, Vn, recheck, sent, rw,
-                                      [&](int j, int c) { return ((cm[j] >> c) & 1u) != 0u; });
-            }
-        };
+        PullCtx pc;
+        pc.rp = p.rp;
+        pc.masks = p.masks;
+        pc.rows4 = rows4;
+        pc.Fd8 = Fd8;
+        pc.SL = p.SL;
+        pc.Q = Qc;
+        pc.tail_ctr = &p.ctl[7];
+        pc.W = recheck ? Vc : Vn;
+        pc.Vn = Vn;
+        pc.len = len;
+        pc.S = S;
+        pc.sent = (uint32_t)vwords;  // sentinel word (all ones) after the bitmap
+        pc.recheck = recheck;
+        pc.tail_div = p.tail_div;
+        pc.gw = gw;
+        pc.NW = NW;
+        pc.all_warps = all_warps;
+        pc.pol = pol;
         if (len < p.dense_min) {
-            // ---- sparse level: every warp expands its own contiguous share of the queue
-            // and pulls it straight from registers — no materialised queue, no barrier ----
-            if (SIGMA)
-                for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
-            if (gw < NW) {
-                const uint64_t lo = (uint64_t)gw * len / NW, hi = (uint64_t)(gw + 1) * len / NW;
-                if (lo < hi) {
-                    SetWindow win;
-                    load_window(p, Fd8, find_set(p, S, lo), S, len, win);
-                    for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
-                        const unsigned long long mine = entry_at(c0, win);
-                        const uint32_t cnt = (hi - c0 < 32) ? (uint32_t)(hi - c0) : 32u;
-                        for (uint32_t k = 0; k < cnt; k += kBatchLazy) {
-                            unsigned long long e = __shfl_sync(0xffffffffu, mine, (lane + k) & 31);
-                            if (lane >= (uint32_t)kBatchLazy || k + lane >= cnt) e = 0;  // absent
-                            pull_batch(e);
-                        }
-                    }
-                }
-            }
-        } else {
-            // ---- dense level: expand SL into the queue, equal contiguous share per warp ----
-            {
-                const uint64_t lo = (uint64_t)gw * len / all_warps, hi = (uint64_t)(gw + 1) * len / all_warps;
-                if (lo < hi) {
-                    SetWindow win;
-                    load_window(p, Fd8, find_set(p, S, lo), S, len, win);
-                    for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
-                        const unsigned long long e = entry_at(c0, win);
-                        if (c0 + lane < hi) Qc[c0 + lane] = e;
-                    }
-                }
-            }
             if (SIGMA)  // Fn is the previous level's α: its readers finished long ago
                 for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
+            ctr[2] += pull_sparse<PULL>(pc);
+        } else {
+            expand_queue(pc);
+            if (SIGMA)
+                for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
             grid_barrier(p.bar, gen);
-
             // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
-            if (gw < NW) {
-                // Batches of kBatchLazy queue positions q0, q0+qs, ... < qe: mask words and row
-                // ids loaded together (streaming loads), the next batch's queue entries fetched
-                // while this batch is processed.
-                auto run = [&](uint64_t q0, uint64_t qs, uint64_t qe) {
-                    const uint64_t step = qs * kBatchLazy;
-                    auto qload = [&](uint64_t base) -> unsigned long long {
-                        const uint64_t pos = base + (uint64_t)lane * qs;
-                        return (lane < kBatchLazy && pos < qe) ? Qc[pos] : 0ull;  // 0: absent
-                    };
-                    unsigned long long e_next = qload(q0);
-                    for (uint64_t p0 = q0; p0 < qe; p0 += step) {
-                        const unsigned long long e = e_next;
-                        e_next = qload(p0 + step);
-                        pull_batch(e);
-                    }
-                };
-                // Positions [0, len - tail): round-robin over the warps like the reference
-                // (p ≡ warp mod #warps, :190). The last 1/tail_div (8; whole grid) is handed
-                // out in chunks of 32 consecutive positions from a counter, so warps that
-                // finish early absorb the tail instead of waiting at the barrier.
-                const uint64_t tail = (NW == all_warps && p.tail_div) ? len / p.tail_div : 0;
-                const uint64_t stat = len - tail;
-                run(gw, NW, stat);
-                if (tail) {
-                    for (;;) {
-                        unsigned long long c = 0;
-                        if (lane == 0) c = atomicAdd(&p.ctl[7], 32ull);
-                        c = __shfl_sync(0xffffffffu, c, 0);
-                        if (c >= tail) break;
-                        run(stat + c, 1, stat + min(c + 32, (unsigned long long)tail));
-                    }
-                }
-            }
+            ctr[2] += pull_dense<PULL>(pc);
         }
         level_barrier(p, sm, gen, level, ctr, 1);
 

@@ -27,6 +27,7 @@
 // counts (tagged with the level) and sums its predecessors'; pass B writes its SL entries.
 #include "bfs.cuh"
 #include "bfs_device.cuh"
+#include "lazy_pull.cuh"
 
 namespace blestgpu {
 
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
             // producer
             if (nst) {
                 SetWindow win;
-                load_window(p, Fd8, find_set(p, S, lo), S, T, win);
+                load_window(p.SL, p.rp, Fd8, find_set(p.SL, S, lo), S, T, win);
                 for (uint32_t i = 0; i < nst; ++i) {
                     const uint32_t g = ring_base + i, s = g % kNS;
                     const uint64_t sp = lo + (uint64_t)i * kSB;
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(32 * (NC + 1)) k_bfs_lazy_tma(Params p) {
                     if (sp + cnt - 1 >= win.wend) {  // slide the window to the set holding sp
                         const unsigned own = __ballot_sync(0xffffffffu, win.first <= sp);
                         const uint32_t nb = (sp >= win.wend) ? win.base + 32 : win.base + (31 - __clz(own));
-                        load_window(p, Fd8, nb, S, T, win);
+                        load_window(p.SL, p.rp, Fd8, nb, S, T, win);
                     }
                     // lane j < kSB resolves position sp + j: binary search of the
                     // window's first positions (5 shuffle steps, all lanes at once)

@@ -12,36 +12,16 @@
 #include "graph.cuh"
 #include "io.cuh"
 #include "ordering.cuh"
+#include "rows.cuh"
 
 using namespace blestgpu;
 
 struct blest_graph_s {
     DeviceGraph g;
 };
-namespace blestgpu {
-struct PartEngine;
-PartEngine* part_create(const DeviceBvss& b);
-void part_destroy(PartEngine* e);
-void part_range(const PartEngine& e, uint32_t* row_lo, uint32_t* row_hi, uint64_t* w_lo, uint64_t* w_hi);
-uint64_t part_begin(PartEngine& e, uint32_t src);
-void part_pull(PartEngine& e, uint64_t len);
-uint64_t part_sweep(PartEngine& e, uint32_t level, uint32_t* diff_out_dev);
-uint64_t part_enqueue(PartEngine& e, const uint32_t* full_diff_dev, uint64_t* total_bits);
-void part_levels(const PartEngine& e, uint32_t* levels_host);
-struct PartDel {
-    void operator()(PartEngine* e) const { part_destroy(e); }
-};
-}  // namespace blestgpu
-
 struct blest_bvss_s {
     DeviceBvss b;
     std::unique_ptr<BfsEngine> engine;
-    std::unique_ptr<PartEngine, PartDel> part;
-    uint64_t part_len = 0;
-    PartEngine& pe() {
-        if (!part) part.reset(part_create(b));
-        return *part;
-    }
     std::vector<uint64_t> last_phase_ns;
     BfsEngine& eng() {
         if (!engine) engine = std::make_unique<BfsEngine>(b);
@@ -460,48 +440,142 @@ int blest_bvss_build_rows(blest_graph g, uint32_t row_lo, uint32_t row_hi, blest
     API_END
 }
 
-int blest_part_range(blest_bvss b, uint32_t* row_lo, uint32_t* row_hi, uint64_t* word_lo, uint64_t* word_hi) {
+struct blest_rows_s {
+    DeviceBvss b;
+    std::unique_ptr<RowsEngine> e;
+};
+
+int blest_partition_rows(blest_graph g, uint32_t world, uint64_t* word_bounds, uint64_t* slices) {
     API_BEGIN
-    NEED(b, "null bvss");
-    part_range(b->pe(), row_lo, row_hi, word_lo, word_hi);
+    NEED(g && word_bounds, "null argument");
+    NEED(world >= 1, "world size must be positive");
+    std::vector<uint64_t> sl;
+    const auto bounds = partition_rows_by_slices(g->g, world, slices ? &sl : nullptr);
+    std::memcpy(word_bounds, bounds.data(), (world + 1) * 8);
+    if (slices) std::memcpy(slices, sl.data(), world * 8);
     API_END
 }
 
-int blest_part_begin(blest_bvss b, uint32_t src, uint64_t* queue_len) {
+int blest_rows_create(blest_graph g, uint32_t rank, uint32_t world, const uint64_t* word_bounds, blest_rows* out) {
     API_BEGIN
-    NEED(b, "null bvss");
-    b->part_len = part_begin(b->pe(), src);
-    if (queue_len) *queue_len = b->part_len;
+    NEED(g && word_bounds && out, "null argument");
+    NEED(world >= 1 && rank < world, "rank out of range");
+    require_device();
+    std::vector<uint64_t> bounds(word_bounds, word_bounds + world + 1);
+    const uint64_t words = ((uint64_t)g->g.n + 31) / 32;
+    NEED(bounds[0] == 0 && bounds[world] == words, "word bounds must span [0, ceil(n/32)]");
+    for (uint32_t r = 0; r < world; ++r) NEED(bounds[r] <= bounds[r + 1], "word bounds must be ascending");
+    auto h = std::make_unique<blest_rows_s>();
+    const uint64_t lo = std::min<uint64_t>(32 * bounds[rank], g->g.n), hi = std::min<uint64_t>(32 * bounds[rank + 1], g->g.n);
+    h->b = bvss_build(g->g, (uint32_t)lo, (uint32_t)hi);
+    h->e = std::make_unique<RowsEngine>(h->b, rank, world, bounds);
+    *out = h.release();
     API_END
 }
 
-int blest_part_pull(blest_bvss b) {
+int blest_rows_info(blest_rows r, uint32_t* row_lo, uint32_t* row_hi, uint32_t* num_vss, uint64_t* per_words) {
     API_BEGIN
-    NEED(b, "null bvss");
-    part_pull(b->pe(), b->part_len);
+    NEED(r, "null engine");
+    if (row_lo) *row_lo = r->e->row_lo();
+    if (row_hi) *row_hi = r->e->row_hi();
+    if (num_vss) *num_vss = r->b.num_vss;
+    if (per_words) *per_words = r->e->per_words();
     API_END
 }
 
-int blest_part_sweep(blest_bvss b, uint32_t level, uint32_t* diff_out, uint64_t* discovered) {
+int blest_rows_ipc_handle(blest_rows r, void* handle64) {
     API_BEGIN
-    NEED(b && diff_out, "null argument");
-    const uint64_t d = part_sweep(b->pe(), level, diff_out);
-    if (discovered) *discovered = d;
+    NEED(r && handle64, "null argument");
+    r->e->ipc_handle(handle64);
     API_END
 }
 
-int blest_part_enqueue(blest_bvss b, const uint32_t* full_diff, uint64_t* queue_len, uint64_t* total_discovered) {
+int blest_rows_open_peers(blest_rows r, const void* handles) {
     API_BEGIN
-    NEED(b && full_diff, "null argument");
-    b->part_len = part_enqueue(b->pe(), full_diff, total_discovered);
-    if (queue_len) *queue_len = b->part_len;
+    NEED(r && handles, "null argument");
+    r->e->open_peers(handles);
     API_END
 }
 
-int blest_part_levels(blest_bvss b, uint32_t* levels_out) {
+namespace {
+std::vector<RowsEngine*> rank_group(blest_rows* ranks, uint32_t world) {
+    std::vector<RowsEngine*> v(world);
+    for (uint32_t i = 0; i < world; ++i) {
+        if (!ranks[i]) throw InvalidArgument("null engine in the rank group");
+        v[i] = ranks[i]->e.get();
+    }
+    return v;
+}
+}  // namespace
+
+int blest_rows_set_local_peers(blest_rows* ranks, uint32_t world) {
     API_BEGIN
-    NEED(b && levels_out, "null argument");
-    part_levels(b->pe(), levels_out);
+    NEED(ranks && world, "null argument");
+    const auto v = rank_group(ranks, world);
+    for (auto* e : v) e->set_local_peers(v);
+    API_END
+}
+
+int blest_rows_bfs(blest_rows r, uint32_t src) {
+    API_BEGIN
+    NEED(r, "null engine");
+    r->e->launch_fused(src);
+    API_END
+}
+
+int blest_rows_group_bfs(blest_rows* ranks, uint32_t world, uint32_t src) {
+    API_BEGIN
+    NEED(ranks && world, "null argument");
+    rows_group_launch(rank_group(ranks, world), src);
+    API_END
+}
+
+int blest_rows_step(blest_rows r, uint32_t level, uint32_t src, const uint32_t* recv) {
+    API_BEGIN
+    NEED(r, "null engine");
+    r->e->step(level, src, recv);
+    API_END
+}
+
+int blest_rows_send_buffer(blest_rows r, uint32_t** send) {
+    API_BEGIN
+    NEED(r && send, "null argument");
+    *send = r->e->send_buffer();
+    API_END
+}
+
+int blest_rows_flags(blest_rows r, uint32_t* progress, uint32_t* done, uint32_t* status) {
+    API_BEGIN
+    NEED(r, "null engine");
+    const volatile unsigned* f = r->e->host_flags();
+    if (progress) *progress = f[0];
+    if (done) *done = f[1];
+    if (status) *status = f[2];
+    API_END
+}
+
+int blest_rows_finish(blest_rows r, uint32_t* levels_owned, blest_rows_stats* out) {
+    API_BEGIN
+    NEED(r, "null engine");
+    const RowsEngine::Stats s = r->e->finish(levels_owned);
+    if (out) {
+        out->iterations = s.iterations;
+        out->max_level = s.max_level;
+        out->queue = s.queue;
+        out->discovered = s.discovered;
+        out->relaxed = s.relaxed;
+        out->pushes = s.pushes;
+    }
+    API_END
+}
+
+int blest_rows_free(blest_rows r) {
+    API_BEGIN
+    if (r) {
+        CK(cudaStreamSynchronize(stream()));
+        r->e.reset();
+        delete r;
+    }
     API_END
 }
 

@@ -1,6 +1,9 @@
-"""TEST INFRASTRUCTURE: a numpy backend of the row-partitioned BFS protocol
-(paper_2512_21967_b200/multigpu.py), built on the oracle's BVSS builder over the
-row-filtered graph. Used by the gloo (CPU, world_size 2) tests of the multi-GPU host logic."""
+"""TEST INFRASTRUCTURE: a numpy backend of the row-partitioned BFS in stepped mode
+(paper_2512_21967_b200/multigpu.py SteppedBfs; csrc/rows.cu k_bfs_rows<STEPPED>), built on
+the oracle's BVSS builder over the row-filtered graph. Same step semantics as the GPU
+engine: step(1) initialises and runs level 1; step(l > 1) unpacks the gathered frontier,
+stops if it is empty (done = l - 1), else runs level l; every level ends with the owned
+diff words in the send buffer. Used by the gloo (CPU, world_size 2/3) protocol tests."""
 import numpy as np
 import torch
 
@@ -16,44 +19,71 @@ def rows_graph(g, lo, hi):
     return O.from_edges(g.n, src[keep], g.targets[keep], directed=True)
 
 
-class NumpyPartition:
-    def __init__(self, g, lo, hi, per_words):
-        self.g, self.lo, self.hi, self.per = g, lo, hi, per_words
-        self.b = O.build_bvss(rows_graph(g, lo, hi))
+class NumpyRows:
+    def __init__(self, g, rank, bounds):
+        self.g, self.rank, self.bounds = g, rank, list(bounds)
+        self.world = len(bounds) - 1
+        self.w_lo, self.w_hi = bounds[rank], bounds[rank + 1]
+        self.row_lo, self.row_hi = min(32 * self.w_lo, g.n), min(32 * self.w_hi, g.n)
+        self.per = max(1, max(b - a for a, b in zip(bounds, bounds[1:])))
+        self.b = O.build_bvss(rows_graph(g, self.row_lo, self.row_hi))
         self.words = (g.n + 31) // 32
-        self.w_lo = lo // 32
+        self._send = torch.zeros(self.per, dtype=torch.int32)
+        self.progress = self.done = self.status = 0
 
-    def row_range(self):
-        return self.lo, self.hi
+    def send(self):
+        return self._send
 
-    def begin(self, src):
-        self.L = np.full(self.g.n, INF, np.uint32)
-        self.Vc = np.zeros(self.words, np.uint32)
-        self.Vn = np.zeros(self.words, np.uint32)
-        if self.lo <= src < self.hi:
-            self.L[src] = 0
-            self.Vc[src >> 5] |= np.uint32(1 << (src & 31))
-            self.Vn[src >> 5] |= np.uint32(1 << (src & 31))
-        ss = src >> 3
-        self.queue = [(v, 1 << (src & 7)) for v in range(self.b.real_ptrs[ss], self.b.real_ptrs[ss + 1])]
-        return len(self.queue)
+    def flags(self):
+        return self.progress, self.done, self.status
 
-    def pull(self):
+    def _queue(self, F):
+        q = []
+        for w in np.flatnonzero(F):
+            for s in range(4):
+                a = (int(F[w]) >> (8 * s)) & 0xFF
+                if a:
+                    ss = 4 * int(w) + s
+                    q += [(v, a) for v in range(self.b.real_ptrs[ss], self.b.real_ptrs[ss + 1])]
+        return q
+
+    def step(self, level, src, recv):
+        if level > 1 and self.done:
+            return  # no-op past the end
+        self.progress = level
+        if level == 1:
+            self.done = self.status = 0
+            self.L = np.full(self.g.n, INF, np.uint32)
+            self.Vc = np.zeros(self.words, np.uint32)
+            self.Vn = np.zeros(self.words, np.uint32)
+            if self.row_lo <= src < self.row_hi:
+                self.L[src] = 0
+                self.Vc[src >> 5] |= np.uint32(1 << (src & 31))
+                self.Vn[src >> 5] |= np.uint32(1 << (src & 31))
+            F = np.zeros(self.words, np.uint32)
+            F[src >> 5] = np.uint32(1 << (src & 31))
+            self.queue_total = 0
+        else:
+            rv = recv.numpy().view(np.uint32)
+            F = np.concatenate([rv[r * self.per: r * self.per + (self.bounds[r + 1] - self.bounds[r])]
+                                for r in range(self.world)])
+            if not F.any():
+                self.done = level - 1
+                return
+        # stage 1 over the local queue (lazy pull: test V_next, mark V_next)
         m = self.b.masks.reshape(-1, 32)
-        r = self.b.row_ids.reshape(-1, 32, 4)
-        for v, a in self.queue:
+        rws = self.b.row_ids.reshape(-1, 32, 4)
+        q = self._queue(F)
+        self.queue_total += len(q)
+        for v, a in q:
             for c in range(4):
                 hit = ((m[v] >> np.uint32(8 * c)) & np.uint32(a)) != 0
-                for u in r[v, hit, c]:
+                for u in rws[v, hit, c]:
                     u = int(u)
-                    bit = np.uint32(1 << (u & 31))
-                    if not (self.Vc[u >> 5] & bit):
-                        self.Vn[u >> 5] |= bit
-
-    def sweep(self, level):
-        whi = (self.hi + 31) // 32
-        diff = self.Vn[self.w_lo:whi] & ~self.Vc[self.w_lo:whi]
-        self.Vc[self.w_lo:whi] |= diff
+                    self.Vn[u >> 5] |= np.uint32(1 << (u & 31))
+        # stage 2a: owned words
+        diff = self.Vn[self.w_lo:self.w_hi] & ~self.Vc[self.w_lo:self.w_hi]
+        self.Vc[self.w_lo:self.w_hi] |= diff
         for k, d in enumerate(diff):
             d = int(d)
             while d:
@@ -62,18 +92,10 @@ class NumpyPartition:
                 self.L[32 * (self.w_lo + k) + b] = level
         out = np.zeros(self.per, np.uint32)
         out[: len(diff)] = diff
-        return torch.from_numpy(out.view(np.int32).copy())
+        self._send = torch.from_numpy(out.view(np.int32).copy())
 
-    def enqueue(self, full):
-        d = full.numpy().view(np.uint32)[: self.words]
-        self.queue = []
-        for w in np.flatnonzero(d):
-            for s in range(4):
-                a = (int(d[w]) >> (8 * s)) & 0xFF
-                if a:
-                    ss = 4 * int(w) + s
-                    self.queue += [(v, a) for v in range(self.b.real_ptrs[ss], self.b.real_ptrs[ss + 1])]
-        return len(self.queue), int(sum(bin(int(x)).count("1") for x in d))
-
-    def levels(self):
-        return self.L[self.lo:self.hi].copy()
+    def finish(self, levels=True):
+        from paper_2512_21967_b200.multigpu import RowsResult
+        lv = self.L[self.row_lo:self.row_hi].copy()
+        disc = int(np.count_nonzero((lv != INF) & (lv != 0)))
+        return RowsResult(lv, self.row_lo, self.row_hi, self.done, disc, self.queue_total)
