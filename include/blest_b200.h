@@ -279,6 +279,9 @@ int blest_rows_send_buffer(blest_rows r, uint32_t** send);
 int blest_rows_flags(blest_rows r, uint32_t* progress, uint32_t* done, uint32_t* status);
 /* Waits for the stream; owned rows' levels (host, row_hi-row_lo entries; may be NULL). */
 int blest_rows_finish(blest_rows r, uint32_t* levels_owned, blest_rows_stats* out);
+/* Level timeline of the last fused BFS (%globaltimer ns; 4 per level: start, stage-1 end,
+ * exchange end, level end); *rows = levels recorded. */
+int blest_rows_phase_times(blest_rows r, uint64_t* out, uint32_t cap, uint32_t* rows);
 int blest_rows_free(blest_rows r);
 
 #ifdef __cplusplus

@@ -166,6 +166,7 @@ SIGNATURES = {
     "blest_rows_flags": (i32, [vp, P(u32), P(u32), P(u32)]),
     "blest_rows_finish": (i32, [vp, vp, P(RowsStatsT)]),
     "blest_rows_free": (i32, [vp]),
+    "blest_rows_phase_times": (i32, [vp, vp, u32, P(u32)]),
 }
 
 _lib = None

@@ -569,6 +569,15 @@ int blest_rows_finish(blest_rows r, uint32_t* levels_owned, blest_rows_stats* ou
     API_END
 }
 
+int blest_rows_phase_times(blest_rows r, uint64_t* out, uint32_t cap, uint32_t* rows) {
+    API_BEGIN
+    NEED(r && out && rows, "null argument");
+    const auto t = r->e->phase_times(cap);
+    std::memcpy(out, t.data(), t.size() * 8);
+    *rows = (uint32_t)(t.size() / 4);
+    API_END
+}
+
 int blest_rows_free(blest_rows r) {
     API_BEGIN
     if (r) {

@@ -95,6 +95,21 @@ struct PullCtx {
     uint64_t pol;                        // L2 evict-first policy for the BVSS stream
 };
 
+// Every pointer of the context addresses global memory. Callers whose pointers come from a
+// struct in global memory (the row-partitioned kernel's per-rank parameters) would
+// otherwise get generic LD instead of LDG for the visited tests and queue reads.
+__device__ __forceinline__ void assume_global(const PullCtx& c) {
+    __builtin_assume(__isGlobal(c.rp));
+    __builtin_assume(__isGlobal(c.masks));
+    __builtin_assume(__isGlobal(c.rows4));
+    __builtin_assume(__isGlobal(c.Fd8));
+    __builtin_assume(__isGlobal(c.SL));
+    __builtin_assume(__isGlobal(c.Q));
+    __builtin_assume(__isGlobal(c.tail_ctr));
+    __builtin_assume(__isGlobal(c.W));
+    __builtin_assume(__isGlobal(c.Vn));
+}
+
 // One warp's view of 32 consecutive SL entries.
 struct SetWindow {
     uint32_t base;   // SL index held by lane 0
@@ -198,6 +213,7 @@ __device__ __forceinline__ uint32_t pull_batch(const PullCtx& c, unsigned long l
 // straight from registers — no materialised queue, no barrier. Returns REDs issued.
 template <int PULL>
 __device__ __forceinline__ uint32_t pull_sparse(const PullCtx& c) {
+    assume_global(c);
     uint32_t reds = 0;
     if (c.gw >= c.NW) return 0;
     const unsigned lane = lane_id();
@@ -221,6 +237,7 @@ __device__ __forceinline__ uint32_t pull_sparse(const PullCtx& c) {
 // grid (a hub set with thousands of VSSs is spread over all warps). A grid barrier must
 // follow before pull_dense.
 __device__ __forceinline__ void expand_queue(const PullCtx& c) {
+    assume_global(c);
     const unsigned lane = lane_id();
     const uint64_t lo = (uint64_t)c.gw * c.len / c.all_warps, hi = (uint64_t)(c.gw + 1) * c.len / c.all_warps;
     if (lo >= hi) return;
@@ -239,6 +256,7 @@ __device__ __forceinline__ void expand_queue(const PullCtx& c) {
 // counter, so warps that finish early absorb the tail instead of waiting at the barrier.
 template <int PULL>
 __device__ __forceinline__ uint32_t pull_dense(const PullCtx& c) {
+    assume_global(c);
     uint32_t reds = 0;
     if (c.gw >= c.NW) return 0;
     const unsigned lane = lane_id();

@@ -47,6 +47,7 @@ struct RowsParams {
     unsigned long long* ctl;
     unsigned long long* agg;   // 3 × 4096: per-CTA (level << 40 | VSS), (… | sets), (… | bits)
     unsigned long long* trace;
+    unsigned long long* tstamp;  // 4 per level (timeline), may be null
     unsigned* hflags;          // mapped host flags
 };
 
@@ -259,16 +260,32 @@ __device__ __forceinline__ void stage2a(const RowsParams& p, uint32_t level, uin
     }
 }
 
+// Per-level counters into the trace row: warp sums, then one shared-memory sum per CTA, then
+// one atomic per CTA and counter (not per warp: 4.7 K same-address atomics per level cost
+// tens of µs).
 template <int THREADS>
-__device__ __forceinline__ void trace_add(const RowsParams& p, uint32_t level, uint32_t (&ctr)[4]) {
-    const uint32_t row = min(level - 1, p.trace_cap - 1);
-    unsigned long long* t = p.trace + 8ull * row;
+__device__ __forceinline__ void trace_add(const RowsParams& p, Smem<THREADS, 1>& sm, uint32_t level, uint32_t (&ctr)[4]) {
+    if (threadIdx.x < 4) sm.ctr[threadIdx.x] = 0;
+    __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t s = warp_sum(ctr[i]);
-        if (lane_id() == 0 && s) atomicAdd(&t[i == 0 ? 3 : (i == 1 ? 4 : (i == 2 ? 6 : 7))], (unsigned long long)s);
+        if (lane_id() == 0 && s) atomicAdd(&sm.ctr[i], (unsigned long long)s);
         ctr[i] = 0;
     }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const unsigned long long s = sm.ctr[threadIdx.x];
+        const uint32_t row = min(level - 1, p.trace_cap - 1);
+        constexpr int slot[4] = {3, 4, 6, 7};  // discovered, full, relaxed, pushes
+        if (s) atomicAdd(&p.trace[8ull * row + slot[threadIdx.x]], s);
+    }
+}
+
+// Level timeline (rank 0's first CTA, %globaltimer): [start, stage-1 end, exchange end, level end].
+__device__ __forceinline__ void stamp(const RowsParams& p, uint32_t vb, uint32_t level, int slot) {
+    if (vb == 0 && threadIdx.x == 0 && p.tstamp && level - 1 < p.trace_cap)
+        p.tstamp[4ull * (level - 1) + slot] = globaltimer();
 }
 
 template <int PULL, int THREADS, bool STEPPED>
@@ -276,6 +293,13 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const Rows
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
     const RowsParams p = P[blockIdx.x / cpr];
+    // the parameters come from global memory, so their pointers would otherwise be generic
+    // (LD/ST instead of LDG/STG/RED everywhere)
+    __builtin_assume(__isGlobal(p.rp) && __isGlobal(p.masks) && __isGlobal(p.rows4) && __isGlobal(p.L));
+    __builtin_assume(__isGlobal(p.Vc) && __isGlobal(p.Vn) && __isGlobal(p.X) && __isGlobal(p.peers));
+    __builtin_assume(__isGlobal(p.Q) && __isGlobal(p.SL) && __isGlobal(p.ctl) && __isGlobal(p.agg));
+    __builtin_assume(__isGlobal(p.trace) && __isGlobal(p.bounds));
+    if (STEPPED) __builtin_assume(__isGlobal(p.send) && __isGlobal(p.recv) && __isGlobal(p.hflags));
     const uint32_t vb = blockIdx.x % cpr, vG = cpr;
     const unsigned lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
@@ -332,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const Rows
         // ---- stepped, level > 1: unpack the gathered frontier, 2b ----
         stage2b<THREADS, STEPPED>(p, sm, level - 1, vb, vG, nullptr, ctr);
         grid_sync();
-        trace_add<THREADS>(p, level - 1, ctr);
+        trace_add<THREADS>(p, sm, level - 1, ctr);
         if (ld_relaxed_gpu_u64(&p.ctl[kBits]) == 0) {  // level - 1 discovered nothing anywhere
             if (gtid == 0) {
                 p.ctl[kIters] = level - 1;
@@ -362,6 +386,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const Rows
             break;
         }
         const uint32_t* Fd = p.X + (STEPPED ? 0 : ((level - 1) & 1) * p.xstride);  // α words
+        stamp(p, vb, level, 0);
         if (gtid == 0) {
             p.ctl[kTail] = 0;
             if (level - 1 < p.trace_cap) {
@@ -400,11 +425,12 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const Rows
             ctr[2] += pull_dense<PULL>(pc);
         }
         grid_sync();
+        stamp(p, vb, level, 1);
 
         // ---- stage 2a: owned words; diffs to the exchange ----
         if (STEPPED) {
             stage2a(p, level, gtid, gthreads, ctr, [&](uint64_t w, uint32_t d) { p.send[w - p.w_lo] = d; });
-            trace_add<THREADS>(p, level, ctr);
+            trace_add<THREADS>(p, sm, level, ctr);
             return;  // host: all-gather, then the next level's launch
         }
         const uint64_t xo = (uint64_t)(level & 1) * p.xstride;
@@ -420,11 +446,13 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const Rows
         if (stored) __threadfence_system();
         grid_sync();
         if (!cross_rank_barrier(p, vb)) break;
+        stamp(p, vb, level, 2);
 
         // ---- stage 2b: the whole exchanged frontier → termination, next SL ----
         stage2b<THREADS, false>(p, sm, level, vb, vG, p.X + xo, ctr);
         grid_sync();
-        trace_add<THREADS>(p, level, ctr);
+        trace_add<THREADS>(p, sm, level, ctr);
+        stamp(p, vb, level, 3);
     }
     if (!STEPPED && gtid == 0) p.ctl[kIters] = level - 1;
 }
@@ -547,6 +575,7 @@ RowsEngine::RowsEngine(const DeviceBvss& b, uint32_t rank, uint32_t world, const
     CK(cudaMemset(agg_.p, 0, agg_.bytes()));
     trace_cap_ = (uint32_t)std::min<uint64_t>((uint64_t)b.n + 2, 1u << 20);
     trace_.alloc(8ull * trace_cap_);
+    tstamp_.alloc(4ull * trace_cap_);
     peers_.alloc(world);
     std::vector<uintptr_t> self(world, 0);
     self[rank] = reinterpret_cast<uintptr_t>(xbuf_.p);
@@ -624,6 +653,7 @@ void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const 
     p.ctl = ctl_.p;
     p.agg = agg_.p;
     p.trace = trace_.p;
+    p.tstamp = tstamp_.p;
     p.hflags = hflags_dev_;
 }
 
@@ -708,6 +738,15 @@ void rows_group_launch(const std::vector<RowsEngine*>& ranks, uint32_t src) {
     void* args[] = {&pp, &c};
     CK(cudaLaunchCooperativeKernel(g.kern, dim3(cpr * G), dim3(g.threads), args, 0, stream()));
     g_launches.fetch_add(1);
+}
+
+std::vector<uint64_t> RowsEngine::phase_times(uint32_t cap) {
+    unsigned long long it = 0;
+    CK(cudaMemcpy(&it, ctl_.p + kIters, 8, cudaMemcpyDeviceToHost));
+    const uint32_t rows = (uint32_t)std::min<uint64_t>({it, (uint64_t)cap, (uint64_t)trace_cap_});
+    std::vector<uint64_t> out(4ull * rows);
+    if (rows) CK(cudaMemcpy(out.data(), tstamp_.p, out.size() * 8, cudaMemcpyDeviceToHost));
+    return out;
 }
 
 RowsEngine::Stats RowsEngine::finish(uint32_t* levels_owned_host) {

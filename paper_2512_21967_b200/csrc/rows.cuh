@@ -64,6 +64,9 @@ public:
         uint64_t queue = 0, discovered = 0, relaxed = 0, pushes = 0;
     };
     Stats finish(uint32_t* levels_owned_host);
+    // per level of the last BFS (rank 0's timeline in a group launch, %globaltimer ns):
+    // start, stage-1 end, exchange end (fused), level end
+    std::vector<uint64_t> phase_times(uint32_t cap);
     uint32_t row_lo() const { return row_lo_; }
     uint32_t row_hi() const { return row_hi_; }
     uint32_t rank() const { return rank_; }
@@ -82,7 +85,7 @@ private:
     DevBuf<uint32_t> L_, V_;             // levels (global size), V_curr | V_next (global words + sentinel)
     DevBuf<uint32_t> xbuf_;              // exchange: X0 | X1 (xstride each) | arrival counter
     DevBuf<uint32_t> send_;              // stepped: owned diff words (per)
-    DevBuf<unsigned long long> q_, sl_, ctl_, agg_, trace_;
+    DevBuf<unsigned long long> q_, sl_, ctl_, agg_, trace_, tstamp_;
     DevBuf<uintptr_t> peers_;            // [world] peer exchange bases
     DevBuf<RowsParams> dparams_;         // kernel parameters (group launch: one per rank)
     std::vector<void*> opened_;          // IPC mappings to close

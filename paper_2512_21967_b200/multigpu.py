@@ -136,6 +136,14 @@ class RowsEngine:
         L.check(L.lib().blest_rows_flags(self._h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def phase_times(self, cap: int = 4096) -> np.ndarray:
+        """Timeline of the last fused BFS: rows of (start, stage-1 end, exchange end, level
+        end) in %globaltimer ns, one per level."""
+        out = (C.c_uint64 * (4 * cap))()
+        rows = C.c_uint32()
+        L.check(L.lib().blest_rows_phase_times(self._h, C.cast(out, C.c_void_p), cap, C.byref(rows)))
+        return np.array(out[: 4 * rows.value], np.uint64).reshape(-1, 4)
+
     def finish(self, levels: bool = True) -> RowsResult:
         out = np.zeros(max(self.row_hi - self.row_lo, 1), np.uint32) if levels else None
         st = L.RowsStatsT()
