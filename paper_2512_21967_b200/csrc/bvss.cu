@@ -36,6 +36,44 @@ __global__ void k_slice_pairs(const uint64_t* __restrict__ off, const uint32_t* 
     if (lane == 0 && mine) atomicAdd(kept, mine);
 }
 
+// Row-range builds (one multi-GPU rank): only the arcs into [row_lo, row_hi) get a key, so
+// the sort and the reduction run over this rank's share of m, not all of it. Pass 1
+// (out == nullptr) counts them; pass 2 writes them (warp-aggregated slots, any order: the
+// radix sort follows).
+__global__ void k_slice_pairs_rows(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tgt, uint32_t n,
+                                   uint32_t row_lo, uint32_t row_hi, uint64_t* __restrict__ keys,
+                                   uint8_t* __restrict__ bits, unsigned long long* __restrict__ ctr) {
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long mine = 0;
+    for (uint64_t u = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; u < n;
+         u += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint64_t hi = (u >> 3) << 32;
+        const uint8_t bit = (uint8_t)(1u << (u & 7));
+        for (uint64_t i0 = off[u]; i0 < off[u + 1]; i0 += 32) {
+            const uint64_t i = i0 + lane;
+            const uint32_t v = i < off[u + 1] ? tgt[i] : row_hi;
+            const bool in = v >= row_lo && v < row_hi;
+            const unsigned ball = __ballot_sync(0xffffffffu, in);
+            if (!keys) {
+                mine += in;
+                continue;
+            }
+            unsigned long long base = 0;
+            if (lane == 0 && ball) base = atomicAdd(ctr, (unsigned long long)__popc(ball));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) {
+                const uint64_t at = base + __popc(ball & ((1u << lane) - 1u));
+                keys[at] = hi | v;
+                bits[at] = bit;
+            }
+        }
+    }
+    if (!keys) {
+        mine = warp_sum(mine);
+        if (lane == 0 && mine) atomicAdd(ctr, mine);
+    }
+}
+
 struct OrOp {
     __device__ __forceinline__ uint8_t operator()(uint8_t a, uint8_t b) const { return a | b; }
 };
@@ -128,41 +166,56 @@ DeviceBvss bvss_build(const DeviceGraph& g, uint32_t row_lo, uint32_t row_hi) {
         CK(cudaStreamSynchronize(st));
         return b;
     }
-    // 1. (set, row) keys with the column bit, one per arc.
-    DevBuf<uint64_t> keys(m);
-    DevBuf<uint8_t> bits(m);
-    DevBuf<unsigned long long> kept(1);
-    CK(cudaMemsetAsync(kept.p, 0, 8, st));
-    k_slice_pairs<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.off.p, g.tgt.p, g.n, row_lo, row_hi, keys.p,
-                                                                    bits.p, kept.p);
-    CK(cudaGetLastError());
-    radix_pairs(keys, bits, m, all_rows ? 32 + bits_of(b.num_sets) : 64);
-    if (!all_rows) {
+    // 1. (set, row) keys with the column bit, one per arc (row range: one per kept arc).
+    uint64_t mk = m;
+    DevBuf<uint64_t> keys;
+    DevBuf<uint8_t> bits;
+    if (all_rows) {
+        keys.alloc(m);
+        bits.alloc(m);
+        DevBuf<unsigned long long> kept(1);
+        CK(cudaMemsetAsync(kept.p, 0, 8, st));
+        k_slice_pairs<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.off.p, g.tgt.p, g.n, row_lo, row_hi,
+                                                                        keys.p, bits.p, kept.p);
+        CK(cudaGetLastError());
+    } else {
+        DevBuf<unsigned long long> ctr(1);
+        CK(cudaMemsetAsync(ctr.p, 0, 8, st));
+        k_slice_pairs_rows<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.off.p, g.tgt.p, g.n, row_lo, row_hi,
+                                                                             nullptr, nullptr, ctr.p);
+        CK(cudaGetLastError());
         unsigned long long hk = 0;
-        CK(cudaMemcpyAsync(&hk, kept.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&hk, ctr.p, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        mk = hk;
         b.m = hk;
+        if (mk == 0) {
+            CK(cudaStreamSynchronize(st));
+            return b;
+        }
+        keys.alloc(mk);
+        bits.alloc(mk);
+        CK(cudaMemsetAsync(ctr.p, 0, 8, st));
+        k_slice_pairs_rows<<<grid_for((uint64_t)g.n * 32, 256), 256, 0, st>>>(g.off.p, g.tgt.p, g.n, row_lo, row_hi,
+                                                                             keys.p, bits.p, ctr.p);
+        CK(cudaGetLastError());
     }
+    radix_pairs(keys, bits, mk, 32 + bits_of(b.num_sets));
     // 2. OR-reduce by key -> unpadded slices, sorted by (set, row) (R:src/bvss.cpp:75-88).
-    DevBuf<uint64_t> skeys(m);
-    DevBuf<uint8_t> smask(m);
+    DevBuf<uint64_t> skeys(mk);
+    DevBuf<uint8_t> smask(mk);
     DevBuf<unsigned long long> nsl(1);
     {
         size_t temp = 0;
         CK(cub::DeviceReduce::ReduceByKey(nullptr, temp, keys.p, skeys.p, bits.p, smask.p, nsl.p,
-                                          OrOp(), (int64_t)m, st));
+                                          OrOp(), (int64_t)mk, st));
         DevBuf<unsigned char> tmp(temp);
         CK(cub::DeviceReduce::ReduceByKey(tmp.p, temp, keys.p, skeys.p, bits.p, smask.p, nsl.p,
-                                          OrOp(), (int64_t)m, st));
+                                          OrOp(), (int64_t)mk, st));
     }
     unsigned long long ns = 0;
     CK(cudaMemcpyAsync(&ns, nsl.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (!all_rows && ns) {  // the drop keys reduce to one trailing all-ones slice
-        uint64_t last = 0;
-        CK(cudaMemcpy(&last, skeys.p + ns - 1, 8, cudaMemcpyDeviceToHost));
-        if (last == ~0ull) --ns;
-    }
     keys.release();
     bits.release();
     b.num_unpadded = ns;

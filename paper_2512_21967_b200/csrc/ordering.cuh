@@ -17,8 +17,9 @@ struct SocialReport {
 // from device out-degrees, floating-point steps in the reference's order (bit-exact).
 SocialReport classify_social_like(const DeviceGraph& g);
 
-// rcm (R:src/ordering.cpp:246-266): identical permutation; each pseudo-peripheral BFS
-// touches only its component (the reference rescans all n per call, :193, :232).
+// rcm (R:src/ordering.cpp:171-266) on the GPU (rcm.cu): identical permutation; plain BFSs
+// as cooperative launches, the Cuthill-McKee order level by level (parent position,
+// degree, id) with radix sorts instead of the sequential queue.
 std::vector<uint32_t> rcm_forward(const DeviceGraph& g);
 
 // jaccard_with_windows(g, sigma, w, nullptr) (R:src/ordering.cpp:139-166) on the GPU:

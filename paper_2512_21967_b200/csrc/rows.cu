@@ -51,6 +51,14 @@ struct RowsParams {
     unsigned* hflags;          // mapped host flags
 };
 
+// Every rank's parameters of one launch, passed by value (kernel parameter space: constant
+// bank loads, no per-thread copy of a global struct). One entry per rank of the launch.
+constexpr uint32_t kMaxLaunchRanks = 16;
+struct RowsLaunch {
+    RowsParams r[kMaxLaunchRanks];
+};
+static_assert(sizeof(RowsLaunch) <= 4096, "kernel parameter block");
+
 namespace {
 using namespace bfsdev;
 namespace cg = cooperative_groups;
@@ -95,6 +103,7 @@ __device__ bool cross_rank_barrier(const RowsParams& p, uint32_t vb) {
         }
         p.ctl[kXBar] = passed + 1;
     }
+    __syncwarp();
     cg::this_grid().sync();
     if (*abort_word) {
         if (vb == 0 && threadIdx.x == 0) p.ctl[kStatus] = 2;
@@ -280,6 +289,7 @@ __device__ __forceinline__ void trace_add(const RowsParams& p, Smem<THREADS, 1>&
         constexpr int slot[4] = {3, 4, 6, 7};  // discovered, full, relaxed, pushes
         if (s) atomicAdd(&p.trace[8ull * row + slot[threadIdx.x]], s);
     }
+    __syncwarp();
 }
 
 // Level timeline (rank 0's first CTA, %globaltimer): [start, stage-1 end, exchange end, level end].
@@ -289,10 +299,10 @@ __device__ __forceinline__ void stamp(const RowsParams& p, uint32_t vb, uint32_t
 }
 
 template <int PULL, int THREADS, bool STEPPED>
-__global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const RowsParams* __restrict__ P, uint32_t cpr) {
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __grid_constant__ RowsLaunch P, uint32_t cpr) {
     constexpr int WPC = THREADS / 32;
     __shared__ Smem<THREADS, 1> sm;
-    const RowsParams p = P[blockIdx.x / cpr];
+    const RowsParams& p = P.r[blockIdx.x / cpr];
     // the parameters come from global memory, so their pointers would otherwise be generic
     // (LD/ST instead of LDG/STG/RED everywhere)
     __builtin_assume(__isGlobal(p.rp) && __isGlobal(p.masks) && __isGlobal(p.rows4) && __isGlobal(p.L));
@@ -397,6 +407,9 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const Rows
                 for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
         }
         // ---- stage 1: pull of the local VSSs (lazy_pull.cuh) ----
+        // reconverge warp 0 after the single-thread blocks above: a diverged warp would run
+        // the whole pull through the shuffles' divergent fallback (measured: 2x stage 1)
+        __syncwarp();
         PullCtx pc;
         pc.rp = p.rp;
         pc.masks = p.masks;
@@ -663,6 +676,16 @@ struct Geometry {
     int threads;
     uint32_t ctas;
 };
+// Stage 1 of every level pulls contiguous equal shares of the queue (the sparse-level path
+// of lazy_pull.cuh). The dense-level path (materialised queue, round-robin + dynamic tail)
+// measured 1.8x slower in this kernel on C2 (3.7 vs 2.07 ms per BFS at one rank; ncu:
+// identical instruction, L1/L2 and DRAM counts, the difference is warps waiting at the
+// grid barrier after stage 1), so it is only used when BLEST_DENSE_MIN asks for it.
+uint64_t rows_dense_min() {
+    if (const char* d = getenv("BLEST_DENSE_MIN")) return (uint64_t)atoll(d);
+    return ~0ull;
+}
+
 Geometry rows_geometry(bool stepped, int threads) {
     Geometry g;
     g.threads = threads;
@@ -680,14 +703,12 @@ void rows_launch(RowsEngine& e, const RowsParams& hp, bool fused) {
     const Geometry g = rows_geometry(!fused, 512);
     const uint32_t ctas = std::min<uint32_t>(g.ctas, kAggStride);
     RowsParams p = hp;
-    p.dense_min = (uint64_t)ctas * (g.threads / 32) * 8;
-    if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
-    if (!e.dparams_.p) e.dparams_.alloc(1);
-    // stream-ordered: the previous launch has read its parameters before this copy runs
-    CK(cudaMemcpyAsync(e.dparams_.p, &p, sizeof(p), cudaMemcpyHostToDevice, stream()));
+    p.dense_min = rows_dense_min();
+    RowsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.r[0] = p;
     uint32_t cpr = ctas;
-    const RowsParams* pp = e.dparams_.p;
-    void* args[] = {&pp, &cpr};
+    void* args[] = {&L, &cpr};
     CK(cudaLaunchCooperativeKernel(g.kern, dim3(ctas), dim3(g.threads), args, 0, stream()));
     g_launches.fetch_add(1);
     e.ctas_ = ctas;
@@ -717,6 +738,7 @@ void RowsEngine::step(uint32_t level, uint32_t src, const uint32_t* recv) {
 void rows_group_launch(const std::vector<RowsEngine*>& ranks, uint32_t src) {
     const uint32_t G = (uint32_t)ranks.size();
     if (!G) throw InvalidArgument("empty rank group");
+    if (G > kMaxLaunchRanks) throw InvalidArgument("at most 16 virtual ranks per launch");
     for (uint32_t r = 0; r < G; ++r)
         if (ranks[r]->rank_ != r || ranks[r]->world_ != G) throw InvalidArgument("rank group out of order");
     if (src >= ranks[0]->b_.n) throw InvalidArgument("bfs source out of range");
@@ -726,16 +748,14 @@ void rows_group_launch(const std::vector<RowsEngine*>& ranks, uint32_t src) {
     std::vector<RowsParams> hp(G);
     for (uint32_t r = 0; r < G; ++r) {
         ranks[r]->fill_params(hp[r], src, 1, nullptr);
-        hp[r].dense_min = (uint64_t)cpr * (g.threads / 32) * 8;
-        if (const char* d = getenv("BLEST_DENSE_MIN")) hp[r].dense_min = (uint64_t)atoll(d);
+        hp[r].dense_min = rows_dense_min();
         ranks[r]->ctas_ = cpr;
     }
-    RowsEngine& head = *ranks[0];
-    if (head.dparams_.count < G) head.dparams_.alloc(G);
-    CK(cudaMemcpyAsync(head.dparams_.p, hp.data(), G * sizeof(RowsParams), cudaMemcpyHostToDevice, stream()));
-    const RowsParams* pp = head.dparams_.p;
+    RowsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    for (uint32_t r = 0; r < G; ++r) L.r[r] = hp[r];
     uint32_t c = cpr;
-    void* args[] = {&pp, &c};
+    void* args[] = {&L, &c};
     CK(cudaLaunchCooperativeKernel(g.kern, dim3(cpr * G), dim3(g.threads), args, 0, stream()));
     g_launches.fetch_add(1);
 }

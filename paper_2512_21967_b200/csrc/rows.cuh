@@ -87,7 +87,6 @@ private:
     DevBuf<uint32_t> send_;              // stepped: owned diff words (per)
     DevBuf<unsigned long long> q_, sl_, ctl_, agg_, trace_, tstamp_;
     DevBuf<uintptr_t> peers_;            // [world] peer exchange bases
-    DevBuf<RowsParams> dparams_;         // kernel parameters (group launch: one per rank)
     std::vector<void*> opened_;          // IPC mappings to close
     unsigned* hflags_ = nullptr;         // mapped host memory
     unsigned* hflags_dev_ = nullptr;

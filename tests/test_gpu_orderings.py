@@ -87,3 +87,47 @@ def test_auto_routing():
     assert a.plan.strategy == B.OrderingStrategy.JaccardWindows
     assert a.plan.classification.is_social_like and a.chosen_mode == B.EngineMode.Eager
     assert a.bfs.levels[3] == 0 and a.bfs.levels[0] == 1 and a.bfs.visited_count == n
+
+
+@pytest.mark.parametrize("kind", ["urand20", "grid1024", "rmat14_directed", "components"])
+def test_gpu_rcm_at_scale_matches_reference(oracle, kind):
+    """The GPU RCM (csrc/rcm.cu: cooperative plain BFSs for pseudo_peripheral, Cuthill-McKee
+    order level by level with radix sorts) gives the reference's permutation
+    (R:src/ordering.cpp:171-266) at scale: urand-20, a 1024 x 1024 grid (1 K levels), a
+    directed RMAT (symmetrised adjacency) and a graph of many small components."""
+    import time
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    if kind == "urand20":
+        s, d = oracle.gen_urand(1 << 20, 16 << 20, 3)
+        n, directed = 1 << 20, False
+    elif kind == "grid1024":
+        s, d = oracle.gen_grid(1024, 1024)
+        n, directed = 1024 * 1024, False
+        f = oracle.random_relabel(n, 5)
+        s, d = f[s], f[d]
+    elif kind == "rmat14_directed":
+        s, d = oracle.gen_rmat(14, 8, 2)
+        n, directed = 1 << 14, True
+    else:  # paths of 1..9 vertices plus isolated vertices, shuffled ids
+        n, src, dst, v = 20000, [], [], 0
+        rng = np.random.default_rng(1)
+        while v < n - 10:
+            k = int(rng.integers(1, 10))
+            src += list(range(v, v + k - 1))
+            dst += list(range(v + 1, v + k))
+            v += k + int(rng.integers(0, 3))
+        f = rng.permutation(n).astype(np.uint32)
+        s, d = f[np.array(src, np.uint32)], f[np.array(dst, np.uint32)]
+        directed = False
+    rg = oracle.ref_from_edges(n, s, d, directed=directed)
+    c = rg.csr()
+    g = B.Graph.from_csr(n, c.offsets, c.targets, directed=directed)
+    t0 = time.perf_counter()
+    got = B.rcm(g).forward_map()
+    t_gpu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    want = rg.rcm()
+    t_ref = time.perf_counter() - t0
+    assert np.array_equal(got, want), kind
+    print(f"{kind}: GPU rcm {t_gpu:.3f} s, reference {t_ref:.3f} s")
