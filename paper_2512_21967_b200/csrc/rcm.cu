@@ -16,6 +16,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "graph.cuh"
@@ -116,12 +119,17 @@ __global__ void k_reset_levels(const uint32_t* __restrict__ vis, uint64_t count,
         level[vis[i]] = kInf;
 }
 
-// CM step: every vertex u at CM position p in [s, e) claims its unvisited neighbours for
-// level l+1 (the first claimer appends it to nxt) and lowers their parent position to p.
-__global__ void k_cm_claim(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tgt,
-                           const uint32_t* __restrict__ ord, uint64_t s, uint64_t e, uint32_t l,
-                           uint32_t* __restrict__ level, uint32_t* __restrict__ par, uint32_t* __restrict__ nxt,
-                           unsigned long long* __restrict__ cnt) {
+
+// Device-chained CM levels (no host round trip per level): ctl = {s, e, state, stopped
+// level}; state 0 running, 1 done (an empty level), 2 stopped at a level too large for the
+// one-CTA sort (the host sorts it with cub and resumes). Launches after a stop are no-ops.
+enum { kS = 0, kE = 1, kState = 2, kStop = 3 };
+__global__ void k_cm_claim_dev(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tgt,
+                               const uint32_t* __restrict__ ord, const unsigned long long* __restrict__ ctl,
+                               uint32_t l, uint32_t* __restrict__ level, uint32_t* __restrict__ par,
+                               uint32_t* __restrict__ nxt, unsigned long long* __restrict__ cnt) {
+    if (ctl[kState] != 0) return;
+    const uint64_t s = ctl[kS], e = ctl[kE];
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t NW = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -130,8 +138,9 @@ __global__ void k_cm_claim(const uint64_t* __restrict__ off, const uint32_t* __r
         for (uint64_t e0 = off[u]; e0 < off[u + 1]; e0 += 32) {
             const uint64_t i = e0 + lane;
             bool mine = false;
+            uint32_t w = 0;
             if (i < off[u + 1]) {
-                const uint32_t w = tgt[i];
+                w = tgt[i];
                 uint32_t lw = level[w];
                 if (lw == kInf) {
                     lw = atomicCAS(level + w, kInf, l + 1);
@@ -139,11 +148,12 @@ __global__ void k_cm_claim(const uint64_t* __restrict__ off, const uint32_t* __r
                     if (mine) lw = l + 1;
                 }
                 if (lw == l + 1) atomicMin(par + w, (uint32_t)p);
-                if (mine) {
-                    const unsigned long long at = atomicAdd(cnt, 1ull);
-                    nxt[at] = w;
-                }
             }
+            const unsigned ball = __ballot_sync(0xffffffffu, mine);
+            unsigned long long base = 0;
+            if (lane == 0 && ball) base = atomicAdd(cnt, (unsigned long long)__popc(ball));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (mine) nxt[base + __popc(ball & ((1u << lane) - 1u))] = w;
         }
     }
 }
@@ -156,15 +166,68 @@ __global__ void k_cm_keys(const uint32_t* __restrict__ ids, uint64_t c, const ui
     }
 }
 
-__global__ void k_copy_u32(const uint32_t* __restrict__ a, uint64_t c, uint32_t* __restrict__ b) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < c; i += (uint64_t)gridDim.x * blockDim.x)
-        b[i] = a[i];
+// One CTA sorts a small level (c <= kSmallLevel) by (parent position, degree, id) and
+// writes it to ord — the same order as the two stable radix sorts of a large level.
+constexpr uint32_t kSmallLevel = 8192;
+__global__ void __launch_bounds__(1024) k_cm_sort_small(const uint32_t* __restrict__ nxt, unsigned long long* cnt,
+                                                        const uint32_t* __restrict__ par,
+                                                        const uint32_t* __restrict__ deg, uint32_t* __restrict__ ord,
+                                                        unsigned long long* ctl, uint32_t l) {
+    extern __shared__ unsigned long long sk[];  // [kSmallLevel] (par << 32 | deg)
+    uint32_t* sid = reinterpret_cast<uint32_t*>(sk + kSmallLevel);
+    if (ctl[kState] != 0) return;
+    const uint64_t c = *cnt;
+    if (c == 0 || c > kSmallLevel) {  // done, or too large for one CTA: the host takes over
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ctl[kState] = c == 0 ? 1 : 2;
+            ctl[kStop] = l;
+        }
+        return;
+    }
+    uint32_t* out = ord + ctl[kE];
+    uint32_t P = 1;
+    while (P < c) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        if (i < c) {
+            const uint32_t w = nxt[i];
+            sk[i] = ((unsigned long long)par[w] << 32) | deg[w];
+            sid[i] = w;
+        } else {
+            sk[i] = ~0ull;
+            sid[i] = 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const unsigned long long a = sk[i], b = sk[l];
+                    const uint32_t ia = sid[i], ib = sid[l];
+                    const bool gt = a > b || (a == b && ia > ib);
+                    if (gt == up) {
+                        sk[i] = b;
+                        sk[l] = a;
+                        sid[i] = ib;
+                        sid[l] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) out[i] = sid[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ctl[kS] = ctl[kE];
+        ctl[kE] += c;
+        *cnt = 0;
+    }
 }
 
-__global__ void k_forward_from_order(const uint32_t* __restrict__ order, uint32_t n, uint32_t* __restrict__ fwd) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        fwd[order[i]] = (uint32_t)(n - 1 - i);  // reversed CM order (:265): Permutation::from_inverse
-}
+
 
 struct Plain {
     uint32_t ecc;
@@ -176,6 +239,15 @@ struct Plain {
 
 std::vector<uint32_t> rcm_forward(const DeviceGraph& g) {
     cudaStream_t st = stream();
+    const bool trace = getenv("BLEST_RCM_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!trace) return;
+        CK(cudaStreamSynchronize(st));
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[rcm] %s %.3f s\n", what, std::chrono::duration<double>(t1 - t0).count());
+        t0 = t1;
+    };
     const uint32_t n = g.n;
     std::vector<uint32_t> forward(n);
     if (!n) return forward;
@@ -193,15 +265,18 @@ std::vector<uint32_t> rcm_forward(const DeviceGraph& g) {
     }
     DevBuf<uint32_t> deg(n), level(n), par(n), vis(n), ord(n), nxt(n), ids2(n), forward_dev(n);
     DevBuf<uint64_t> keys(n), keys2(n);
-    DevBuf<unsigned long long> ctl(4), key(1), cnt(1);
+    DevBuf<unsigned long long> ctl(4), key(1), cnt(1), cml(4);
+    const uint32_t claim_ctas = 8u * (uint32_t)num_sms();
     DevBuf<unsigned> best(1);
     k_deg_init<<<grid_for(n, 256), 256, 0, st>>>(off, n, deg.p, level.p, par.p);
     CK(cudaGetLastError());
+    lap("symmetrise + init");
     // cub scratch for the per-level sorts, sized once for n items
     size_t t1 = 0, t2 = 0;
     CK(cub::DeviceRadixSort::SortKeys(nullptr, t1, nxt.p, ids2.p, (int64_t)n, 0, 32, st));
     CK(cub::DeviceRadixSort::SortPairs(nullptr, t2, keys.p, keys2.p, ids2.p, nxt.p, (int64_t)n, 0, 64, st));
     DevBuf<unsigned char> tmp(std::max<size_t>({t1, t2, 1}));
+    CK(cudaFuncSetAttribute(k_cm_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmallLevel * 12)));
     // plain BFS: one cooperative launch
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plain_bfs, 256, 0));
@@ -256,22 +331,41 @@ std::vector<uint32_t> rcm_forward(const DeviceGraph& g) {
             best_ecc = r.ecc;
             current = r.next;
         }
+        lap("pseudo_peripheral");
         // Cuthill-McKee order of the component from `current`, level by level
         comps.emplace_back(v, placed);
         const uint32_t one_level = 0;
         CK(cudaMemcpyAsync(ord.p + placed, &current, 4, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(level.p + current, &one_level, 4, cudaMemcpyHostToDevice, st));
         uint64_t s = placed, e = placed + 1;
-        for (uint32_t l = 0;; ++l) {
+        {
+            const unsigned long long init[4] = {s, e, 0, 0};
+            CK(cudaMemcpyAsync(cml.p, init, 32, cudaMemcpyHostToDevice, st));
             CK(cudaMemsetAsync(cnt.p, 0, 8, st));
-            k_cm_claim<<<grid_for((e - s) * 32, 256), 256, 0, st>>>(off, tgt, ord.p, s, e, l, level.p, par.p, nxt.p,
-                                                                     cnt.p);
+        }
+        uint32_t l = 0;
+        constexpr uint32_t kBatchLevels = 64;
+        for (;;) {
+            for (uint32_t k = 0; k < kBatchLevels; ++k) {
+                k_cm_claim_dev<<<claim_ctas, 256, 0, st>>>(off, tgt, ord.p, cml.p, l + k, level.p, par.p, nxt.p,
+                                                           cnt.p);
+                k_cm_sort_small<<<1, 1024, kSmallLevel * 12, st>>>(nxt.p, cnt.p, par.p, deg.p, ord.p, cml.p, l + k);
+            }
             CK(cudaGetLastError());
+            unsigned long long h[4];
+            CK(cudaMemcpyAsync(h, cml.p, 32, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            s = h[kS];
+            e = h[kE];
+            if (h[kState] == 1) break;
+            if (h[kState] == 0) {
+                l += kBatchLevels;
+                continue;
+            }
+            // a large level: ascending id, then a stable sort by (parent position, degree)
             unsigned long long c = 0;
             CK(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            if (!c) break;
-            // ascending id, then a stable sort by (parent position, degree)
             size_t a = tmp.count;
             CK(cub::DeviceRadixSort::SortKeys(tmp.p, a, nxt.p, ids2.p, (int64_t)c, 0, 32, st));
             k_cm_keys<<<grid_for(c, 256), 256, 0, st>>>(ids2.p, c, par.p, deg.p, keys.p);
@@ -280,9 +374,15 @@ std::vector<uint32_t> rcm_forward(const DeviceGraph& g) {
             CK(cub::DeviceRadixSort::SortPairs(tmp.p, a, keys.p, keys2.p, ids2.p, ord.p + e, (int64_t)c, 0, 64, st));
             s = e;
             e += c;
+            const unsigned long long resume[4] = {s, e, 0, 0};
+            CK(cudaMemcpyAsync(cml.p, resume, 32, cudaMemcpyHostToDevice, st));
+            CK(cudaMemsetAsync(cnt.p, 0, 8, st));
+            l = (uint32_t)h[kStop] + 1;
         }
         placed = e;
+        lap("cuthill_mckee");
     }
+    lap("component search");
     // merge the isolated vertices (singleton components) in by id, then reverse
     std::vector<uint32_t> deg_h(n), ord_h(placed);
     CK(cudaMemcpyAsync(deg_h.data(), deg.p, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
@@ -301,6 +401,7 @@ std::vector<uint32_t> rcm_forward(const DeviceGraph& g) {
         }
     }
     if (order.size() != n) throw LogicError("rcm: order does not cover every vertex");
+    lap("merge");
     for (uint32_t i = 0; i < n; ++i) forward[order[i]] = n - 1 - i;
     return forward;
 }
