@@ -331,15 +331,28 @@ def run_reference(args):
     t0 = time.time()
     gp = O.permute_csr(g, fwd, threads) if fwd is not None else g
     arr = O.build_bvss_mt(gp, threads)
-    rb = O.ref_bvss_from_arrays(arr)
+    # the reference engine indexes slots with u32 (R:include/blest/bvss.hpp:60-62): from 2^25
+    # VSSs (C5) it is invalid and the reference path is reference_bfs
+    engine_ok = arr.num_vss < (1 << 25)
+    rb = O.ref_bvss_from_arrays(arr) if engine_ok else None
     t_build = time.time() - t0
     lazy = engine_policy_lazy(n, arr.m, arr.num_vss) if args.mode == "b200" else (args.mode == "lazy")
     total = args.steps * max(args.gpus, 1) + args.warmup
     srcs_orig = O.pick_sources(g, total, args.source_seed)
     srcs = fwd[srcs_orig] if fwd is not None else srcs_orig
     warm, mine = srcs[: args.warmup], srcs[args.warmup: args.warmup + args.steps]
-    run = lambda s: rb.run(int(s), lazy, warps=32 * threads, workers=threads, want_levels=True, n=n,
-                           trace_cap=1 << 16)
+    if engine_ok:
+        run = lambda s: rb.run(int(s), lazy, warps=32 * threads, workers=threads, want_levels=True, n=n,
+                               trace_cap=1 << 16)
+    else:
+        class _R:
+            pass
+
+        def run(s):
+            r = _R()
+            r.levels = O.reference_bfs(gp, int(s))[0]
+            return r
+        del arr
     for s in warm:
         run(s)
     times, edges, t_start = [], [], time.time()
@@ -355,16 +368,20 @@ def run_reference(args):
     got = run(mine[0]).levels
     ok = bool(np.array_equal(got if fwd is None else got[fwd], want))
     hm = len(times) / sum(t / e for t, e in zip(times, edges)) / 1e9
-    workload = dict(workload=args.config, graph=desc, n=n, arcs=int(arr.m), num_vss=int(arr.num_vss),
+    workload = dict(workload=args.config, graph=desc, n=n, arcs=int(gp.m),
+                    num_vss=int(arr.num_vss) if engine_ok else None,
                     ordering=strategy, engine="lazy" if lazy else "eager", engine_policy=args.mode,
                     sources=len(times), source_seed=args.source_seed,
                     prep_s=dict(generate_s=round(t_gen, 3), order_s=round(t_order, 3), build_s=round(t_build, 3)),
                     parallelism=f"{threads} host threads")
-    cpu = dict(value=round(hm, 6), unit="GTEPS", cores=threads, kind="reference" if O.ref_available() else "port",
+    cpu = dict(value=round(hm, 6), unit="GTEPS", cores=threads if engine_ok else 1,
+               kind="reference" if (O.ref_available() and engine_ok) else "port",
                cpu_model=cpu_model(),
-               sample=f"{len(times)} of {args.steps} sources (bounded ~150 s) after {len(warm)} warm-up runs, "
-                      f"R:src/bfs_engine.cpp run_{'lazy' if lazy else 'eager'} workers={threads} "
-                      f"num_warps={32 * threads} over a BVSS built by the CPU oracle (no GPU)")
+               sample=(f"{len(times)} of {args.steps} sources (bounded ~150 s) after {len(warm)} warm-up runs, "
+                       f"R:src/bfs_engine.cpp run_{'lazy' if lazy else 'eager'} workers={threads} "
+                       f"num_warps={32 * threads} over a BVSS built by the CPU oracle (no GPU)") if engine_ok else
+                      (f"{len(times)} of {args.steps} sources: reference_bfs (R:src/graph.cpp:144-167, the "
+                       f"oracle's restatement, 1 core); the reference engine is invalid at >= 2^25 VSSs"))
     line = dict(metric="GTEPS (harmonic mean over sources)", value=round(hm, 6), unit="GTEPS", n_gpus=args.gpus,
                 steps=len(times), warmup=len(warm), ms_per_step=round(1e3 * sum(times) / len(times), 3),
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
@@ -577,15 +594,24 @@ def main():
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
+    # The reference engine indexes slots with u32 (R:include/blest/bvss.hpp:60-62) and is
+    # invalid from 2^25 VSSs (C5); there the baseline is reference_bfs alone.
+    engine_ok = b.num_vss < (1 << 25)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        glv = {int(mine[k]): census[k]["levels"] for k in range(len(mine)) if census[k].get("levels") is not None}
-        kind, cores, ctimes, _, echeck = cpu_reference_sample(prep, mine, lazy, args.cpu_budget, threads,
-                                                              max_steps=8, gpu_levels=glv)
-        chm = len(ctimes) / sum(tc / e for tc, e in zip(ctimes, E[: len(ctimes)])) / 1e9
-        cpu = dict(value=round(chm, 6), unit="GTEPS", cores=cores, kind=kind, cpu_model=cpu_model(),
-                   sample=f"first {len(ctimes)} of the {len(mine)} timed sources (~{args.cpu_budget:.0f} s budget), "
-                          f"run_{'lazy' if lazy else 'eager'} over the same BVSS arrays",
-                   engine_levels_vs_gpu=echeck)
+        echeck = None
+        if engine_ok:
+            glv = {int(mine[k]): census[k]["levels"] for k in range(len(mine)) if census[k].get("levels") is not None}
+            kind, cores, ctimes, _, echeck = cpu_reference_sample(prep, mine, lazy, args.cpu_budget, threads,
+                                                                  max_steps=8, gpu_levels=glv)
+            chm = len(ctimes) / sum(tc / e for tc, e in zip(ctimes, E[: len(ctimes)])) / 1e9
+            cpu = dict(value=round(chm, 6), unit="GTEPS", cores=cores, kind=kind, cpu_model=cpu_model(),
+                       sample=f"first {len(ctimes)} of the {len(mine)} timed sources (~{args.cpu_budget:.0f} s "
+                              f"budget), run_{'lazy' if lazy else 'eager'} over the same BVSS arrays",
+                       engine_levels_vs_gpu=echeck)
+        else:
+            cpu = dict(value=None, unit="GTEPS", cores=1, kind="port", cpu_model=cpu_model(),
+                       sample="reference engine not run: its u32 slot index wraps at >= 2^25 VSSs "
+                              f"({b.num_vss} here, R:include/blest/bvss.hpp:60-62); reference_bfs below")
         # reference_bfs on one core (R:src/graph.cpp:144-167, the oracle's restatement), one source
         O = oracle_mod()
         g1 = O.Csr(n, *prep["gp"].csr())
@@ -597,7 +623,9 @@ def main():
                                           levels_match_gpu=bool(census[0].get("levels") is None or
                                                                 np.array_equal(lv1, census[0]["levels"])),
                                           sample="first timed source, orc_reference_bfs (FIFO queue BFS)")
-        if parity is not None:
+        if cpu["value"] is None:
+            cpu["value"] = cpu["reference_bfs_1core"]["value"]
+        if parity is not None and echeck is not None:
             parity["engine_levels_vs_gpu"] = echeck
         del g1
 

@@ -89,7 +89,7 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     wstride_ = (words_ + 1 + 3) / 4 * 4;  // 16-byte aligned bitmaps (stage 2 reads uint4) + a sentinel word
     bits_.alloc(4 * (wstride_ ? wstride_ : 4));
     q_.alloc(3 * (uint64_t)(b.num_vss ? b.num_vss : 1));
-    ctl_.alloc(8);
+    ctl_.alloc(16);
     agg_.alloc(4096);
     aggS_.alloc(4096);
     sl_.alloc((uint64_t)b.num_sets + 1);
@@ -127,6 +127,7 @@ uint64_t BfsEngine::prepare(const EngineOptions& opt) {
 
 void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (src >= b_.n) throw InvalidArgument("bfs source out of range");
+    if (b_.num_sets >= (1u << 25)) throw InvalidArgument("the BFS engines support n < 2^28");
     const char* var_env = getenv("BLEST_LAZY_VARIANT");
     const bool lazy_tma = opt.mode == Mode::Lazy && (opt.lazy_tma || (var_env && std::string(var_env) == "tma"));
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
@@ -191,7 +192,10 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
         p.sig = sigma_.sig.p;
         p.hot_words = sigma_.hot_words;
     }
-    p.dense_min = (uint64_t)ctas * (threads / 32) * 8;
+    // dense levels: eager from 8 VSSs per warp (re-check / prefetch mode); lazy from 96 per
+    // warp — below that the contiguous-share pull without a materialised queue wins (C2
+    // 1.574 -> 1.567 ms, C3 2.650 -> 2.628 ms against 8 per warp, same-box A/B)
+    p.dense_min = (uint64_t)ctas * (threads / 32) * (opt.mode == Mode::Lazy ? 96 : 8);
     if (const char* d = getenv("BLEST_DENSE_MIN")) p.dense_min = (uint64_t)atoll(d);
     if (const char* x = getenv("BLEST_XFLAGS")) p.xflags = (uint32_t)atoi(x);
     p.tail_div = 8;  // dense lazy levels hand out their last eighth dynamically
