@@ -283,7 +283,8 @@ __device__ __forceinline__ void column_counts(uint32_t m, uint32_t alpha, uint32
 template <int THREADS, int MODE>
 __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS, MODE>& sm, unsigned& gen,
                                                   uint32_t level, uint32_t (&c)[4], int stamp_slot,
-                                                  const unsigned long long* payload = nullptr) {
+                                                  const unsigned long long* payload = nullptr,
+                                                  unsigned long long* red_flag = nullptr) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t s = warp_sum(c[i]);
@@ -299,7 +300,10 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
             sm.ctr[i] = 0;
         }
     }
-    const uint32_t pay = grid_barrier_pay(p.bar, gen, payload);
+    // red_flag: set (plain store, every writer stores 1) when the CTA issued a stage-1 RED;
+    // read back as the payload after the barrier
+    if (red_flag && threadIdx.x == 0 && mine[2]) *red_flag = 1ull;
+    const uint32_t pay = grid_barrier_pay(p.bar, gen, red_flag ? red_flag : payload);
     if (threadIdx.x == 0) {
         const uint32_t row = min(level - 1, p.trace_cap - 1);
         unsigned long long* t = p.trace + 8ull * row;

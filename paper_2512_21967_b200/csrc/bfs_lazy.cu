@@ -59,7 +59,6 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
     const uint32_t sset = src / kSigma;
     const uint32_t seed_b = p.rp[sset], seed_e = p.rp[sset + 1];
     const uint32_t vsrc = SIGMA ? p.sig[src] : src;  // the source's engine id (hot rank or row)
-    for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
     const uint32_t src_word = src >> 5, src_bit = 1u << (src & 31);
     const uint64_t vs_word = vsrc >> 5;
     const uint32_t vs_bit = 1u << (vsrc & 31);
@@ -86,6 +85,10 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         for (int i = 0; i < 8; ++i) p.trace[i] = 0;
     }
     uint32_t next_T = grid_barrier_pay(p.bar, gen, &p.ctl[0]);
+    // The level array (4n bytes, the bulk of init_state) is written after the init barrier:
+    // its stores drain while level 1's stage 1 runs (nothing reads L), and the barrier after
+    // that stage orders them before stage 2's first level stores (~5 µs per BFS).
+    for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
 
     uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
     uint32_t level = 1;
@@ -99,6 +102,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         }
         if (gtid == 0) {
             p.ctl[7] = 0;  // stage-1 tail chunk counter (read after the expansion barrier)
+            p.ctl[2 + ((level + 1) & 1)] = 0;  // the next level's RED flag (last read at level - 1)
             if (level - 1 < p.trace_cap) {
                 p.trace[8ull * (level - 1) + 0] = level;
                 p.trace[8ull * (level - 1) + 1] = len;
@@ -147,7 +151,14 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
             // ---- stage 1: pull (pull_vss, R:src/bfs_engine.cpp:131-146) ----
             ctr[2] += pull_dense<PULL>(pc);
         }
-        level_barrier(p, sm, gen, level, ctr, 1);
+        // No RED this level ⇔ no discovery (a RED is the only way a V_next bit gets set, and
+        // the barrier before the stage made every earlier bit visible to the tests): the
+        // level is the barren last one — skip its Θ(n/32) stage 2 (one per BFS, ~17 µs).
+        if (level_barrier(p, sm, gen, level, ctr, 1, nullptr, &p.ctl[2 + (level & 1)]) == 0) {
+            if (gtid == 0 && level - 1 < p.trace_cap) p.tstamp[3ull * (level - 1) + 2] = globaltimer();
+            ++level;  // the barren level counts as an iteration (R:src/bfs_engine.cpp:117-124)
+            break;
+        }
 
         if (SIGMA)
             lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen, Fn);
