@@ -108,9 +108,19 @@ void BfsEngine::ensure_sigma() {
     if (sigma_built_) return;
     const char* hot = getenv("BLEST_HOT");
     sigma_view_build(b_, sigma_, hot ? (uint32_t)atoll(hot) : 0u);
+    sigma_built_ = true;
+    // BLEST_SIGMA=1 forces the view; otherwise it is kept only where the hot rows hold a
+    // large share of the slots (sigma.cuh kSigmaMinShare) — no engine copy otherwise
+    const char* sig_env = getenv("BLEST_SIGMA");
+    sigma_on_ = (sig_env && atoi(sig_env) == 1) || sigma_.hot_share >= kSigmaMinShare;
+    if (!sigma_on_) {
+        sigma_.rows.release();
+        sigma_.sig.release();
+        sigma_.inv.release();
+        return;
+    }
     const uint64_t stride = sigma_.hot_words + wstride_;  // both multiples of 4 words
     vext_.alloc(2 * stride);
-    sigma_built_ = true;
 }
 
 uint64_t BfsEngine::prepare(const EngineOptions& opt) {
@@ -120,7 +130,7 @@ uint64_t BfsEngine::prepare(const EngineOptions& opt) {
     uint64_t bytes = levels_.count * 4 + levels2_.count * 4 + bits_.count * 4 + q_.count * 8 + ctl_.count * 8 +
                      agg_.count * 8 + aggS_.count * 8 + sl_.count * 8 + bar_.count * 4 + trace_.count * 8 +
                      tstamp_.count * 8;
-    if (sigma_built_)
+    if (sigma_on_)
         bytes += sigma_.rows.count * 4 + sigma_.sig.count * 4 + sigma_.inv.count * 4 + vext_.count * 4;
     return bytes;
 }
@@ -133,7 +143,11 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     const char* nc_env = getenv("BLEST_TMA_CONSUMERS");
     const int consumers = nc_env ? atoi(nc_env) : 8;
     const char* sig_env = getenv("BLEST_SIGMA");
-    const bool sigma = opt.mode == Mode::Lazy && !lazy_tma && opt.sigma && !(sig_env && atoi(sig_env) == 0);
+    bool sigma = opt.mode == Mode::Lazy && !lazy_tma && opt.sigma && !(sig_env && atoi(sig_env) == 0);
+    if (sigma) {
+        ensure_sigma();
+        sigma = sigma_on_;
+    }
     const int threads = lazy_tma ? 32 * (consumers + 1) : (opt.threads ? (int)opt.threads : 512);
     void* kern = nullptr;
     if (opt.mode == Mode::Eager)
@@ -183,7 +197,6 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
     if (sigma) {
-        ensure_sigma();
         const uint64_t stride = sigma_.hot_words + wstride_;
         p.B0 = vext_.p;  // V_curr / V_next = [hot prefix | row words]
         p.B1 = vext_.p + stride;

@@ -94,6 +94,7 @@ private:
     SigmaView sigma_;                    // lazy: hot-row view, built on the first lazy launch
     DevBuf<uint32_t> vext_;              // lazy hot-row view: V_curr, V_next with the hot prefix
     bool sigma_built_ = false;
+    bool sigma_on_ = false;              // view built and worth using (hot share, BLEST_SIGMA)
     DevBuf<unsigned> bar_;               // grid barrier [2]
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
     DevBuf<unsigned long long> tstamp_;  // trace_cap_ * 3

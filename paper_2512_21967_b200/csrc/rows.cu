@@ -48,6 +48,13 @@ struct RowsParams {
     unsigned long long* agg;   // 3 × 4096: per-CTA (level << 40 | VSS), (… | sets), (… | bits)
     unsigned long long* trace;
     unsigned long long* tstamp;  // 4 per level (timeline), may be null
+    // hot-row view of the rank's rows (sigma.cuh; hot_words = 0: plain row ids): V words =
+    // [hot prefix | row words]; inv: hot rank -> row; sig: row -> engine id; H: staging
+    // words (row space) for the hot discoveries of the level
+    uint64_t hot_words;
+    const uint32_t* inv;
+    const uint32_t* sig;
+    uint32_t* H;
     unsigned* hflags;          // mapped host flags
 };
 
@@ -248,14 +255,21 @@ __device__ __forceinline__ void stage2a(const RowsParams& p, uint32_t level, uin
                                         uint32_t (&ctr)[4], Emit emit) {
     const unsigned lane = lane_id();
     const uint64_t span = p.w_hi - p.w_lo;
+    uint32_t* Vc = p.Vc + p.hot_words;  // row words (after the hot prefix)
+    const uint32_t* Vn = p.Vn + p.hot_words;
     for (uint64_t i0 = gtid - lane; i0 < span; i0 += gthreads) {
         const uint64_t w = p.w_lo + i0 + lane;
-        uint32_t d = 0;
+        uint32_t d = 0, out = 0;
         if (i0 + lane < span) {
-            const uint32_t nx = __ldcg(p.Vn + w);
-            d = nx & ~p.Vc[w];
-            if (d) p.Vc[w] = nx;
-            emit(w, d);
+            const uint32_t nx = __ldcg(Vn + w);
+            d = nx & ~Vc[w];
+            if (d) Vc[w] = nx;
+            out = d;
+            if (p.hot_words) {  // the hot rows' discoveries (levels already stored)
+                out |= __ldcg(p.H + w);
+                p.H[w] = 0u;
+            }
+            emit(w, out);
         }
         ctr[0] += __popc(d);
         unsigned ball = __ballot_sync(0xffffffffu, d != 0);
@@ -265,6 +279,24 @@ __device__ __forceinline__ void stage2a(const RowsParams& p, uint32_t level, uin
             const uint32_t dk = __shfl_sync(0xffffffffu, d, k);
             const uint64_t wk = p.w_lo + i0 + k;
             if ((dk >> lane) & 1u) p.L[32 * wk + lane] = level;
+        }
+    }
+}
+
+// Hot pass of stage 2a: the hot prefix of V (word w handled by CTA w mod G): each hot
+// discovery mapped back by σ⁻¹ to store its level and RED its bit into H (row space); the
+// owned-word sweep merges H after a grid barrier.
+__device__ __forceinline__ void stage2a_hot(const RowsParams& p, uint32_t level, uint32_t vb, uint32_t vG,
+                                            uint32_t (&ctr)[4]) {
+    for (uint64_t w = vb + (uint64_t)threadIdx.x * vG; w < p.hot_words; w += (uint64_t)blockDim.x * vG) {
+        const uint32_t nx = __ldcg(p.Vn + w), d = nx & ~p.Vc[w];
+        if (!d) continue;
+        p.Vc[w] = nx;
+        ctr[0] += __popc(d);
+        for (uint32_t rest = d; rest; rest &= rest - 1) {
+            const uint32_t r = __ldg(p.inv + 32 * w + (__ffs(rest) - 1));
+            p.L[r] = level;
+            red_or(p.H + (r >> 5), 1u << (r & 31));
         }
     }
 }
@@ -309,6 +341,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
     __builtin_assume(__isGlobal(p.Vc) && __isGlobal(p.Vn) && __isGlobal(p.X) && __isGlobal(p.peers));
     __builtin_assume(__isGlobal(p.Q) && __isGlobal(p.SL) && __isGlobal(p.ctl) && __isGlobal(p.agg));
     __builtin_assume(__isGlobal(p.trace) && __isGlobal(p.bounds));
+    if (p.hot_words) __builtin_assume(__isGlobal(p.inv) && __isGlobal(p.sig) && __isGlobal(p.H));
     if (STEPPED) __builtin_assume(__isGlobal(p.send) && __isGlobal(p.recv) && __isGlobal(p.hflags));
     const uint32_t vb = blockIdx.x % cpr, vG = cpr;
     const unsigned lane = lane_id();
@@ -316,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
     const uint64_t gtid = vb * (uint64_t)THREADS + threadIdx.x;
     const uint64_t gthreads = (uint64_t)vG * THREADS;
     const uint32_t gw = vb * WPC + warp, all_warps = vG * WPC;
-    const uint32_t sent = (uint32_t)p.words;  // sentinel word index of V (all ones)
+    const uint32_t sent = (uint32_t)(p.hot_words + p.words);  // sentinel word index of V (all ones)
     uint32_t ctr[4] = {0, 0, 0, 0};           // discovered, -, relaxed, pushes
     auto grid_sync = [] { cg::this_grid().sync(); };
 
@@ -328,10 +361,20 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
         // ---- init_state (R:src/bfs_engine.cpp:30-49) restricted to the owned rows ----
         const uint32_t src = p.src, sset = src / kSigma;
         for (uint64_t i = 32 * p.w_lo + gtid; i < 32 * p.w_hi && i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
-        for (uint64_t w = p.w_lo + gtid; w < p.w_hi; w += gthreads) {
-            const uint32_t seed = (w == (src >> 5)) ? 1u << (src & 31) : 0u;
+        // V: the hot prefix and the owned row words; the source's engine id if it is ours
+        const bool own_src = src >= 32 * p.w_lo && src < 32 * p.w_hi;
+        const uint32_t vsrc = own_src ? (p.hot_words ? p.sig[src] : src) : 0xFFFFFFFFu;
+        for (uint64_t w = gtid; w < p.hot_words; w += gthreads) {
+            const uint32_t seed = (own_src && w == (vsrc >> 5)) ? 1u << (vsrc & 31) : 0u;
             p.Vc[w] = seed;
             p.Vn[w] = seed;
+        }
+        for (uint64_t w = p.w_lo + gtid; w < p.w_hi; w += gthreads) {
+            const uint64_t ew = p.hot_words + w;
+            const uint32_t seed = (own_src && ew == (vsrc >> 5)) ? 1u << (vsrc & 31) : 0u;
+            p.Vc[ew] = seed;
+            p.Vn[ew] = seed;
+            if (p.hot_words) p.H[w] = 0u;
         }
         // α of level 1: the source's bit in X0 (every rank); fused: X1 cleared for the peers
         for (uint64_t w = gtid; w < p.words; w += gthreads) {
@@ -441,6 +484,10 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
         stamp(p, vb, level, 1);
 
         // ---- stage 2a: owned words; diffs to the exchange ----
+        if (p.hot_words) {  // same on every rank of a launch: the barrier counts match
+            stage2a_hot(p, level, vb, vG, ctr);
+            grid_sync();
+        }
         if (STEPPED) {
             stage2a(p, level, gtid, gthreads, ctr, [&](uint64_t w, uint32_t d) { p.send[w - p.w_lo] = d; });
             trace_add<THREADS>(p, sm, level, ctr);
@@ -575,7 +622,26 @@ RowsEngine::RowsEngine(const DeviceBvss& b, uint32_t rank, uint32_t world, const
     dbounds_.alloc(world + 1);
     CK(cudaMemcpy(dbounds_.p, bounds_.data(), (world + 1) * 8, cudaMemcpyHostToDevice));
     L_.alloc(b.n ? b.n : 1);
-    V_.alloc(2 * (words_ + 4));
+    // hot-row view of this rank's rows (BLEST_SIGMA=0: plain row ids)
+    const char* sig_env = getenv("BLEST_SIGMA");
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t sigma_bytes = (uint64_t)b.num_vss * kTau * 4 + 8ull * b.n;  // engine row ids + tables
+    if (b.num_vss && !(sig_env && atoi(sig_env) == 0) && sigma_bytes + (4ull << 30) < free_b) {
+        const char* hot = getenv("BLEST_HOT");
+        sigma_view_build(b, sigma_, hot ? (uint32_t)atoll(hot) : 0u);
+        sigma_built_ = (sig_env && atoi(sig_env) == 1) || sigma_.hot_share >= kSigmaMinShare;
+        if (sigma_built_) {
+            H_.alloc(words_ + 4);
+            CK(cudaMemset(H_.p, 0, H_.bytes()));
+        } else {
+            sigma_.rows.release();
+            sigma_.sig.release();
+            sigma_.inv.release();
+        }
+    }
+    vstride_ = (sigma_built_ ? sigma_.hot_words : 0) + (words_ + 4) / 4 * 4 + 4;  // + sentinel, 16 B aligned
+    V_.alloc(2 * vstride_);
     xbuf_.alloc(2 * xstride_ + 4);
     CK(cudaMemset(xbuf_.p, 0, xbuf_.bytes()));
     send_.alloc(per_);
@@ -634,7 +700,7 @@ void RowsEngine::set_local_peers(const std::vector<RowsEngine*>& ranks) {
     CK(cudaMemcpy(peers_.p, bases.data(), world_ * sizeof(uintptr_t), cudaMemcpyHostToDevice));
 }
 
-void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const uint32_t* recv) const {
+void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const uint32_t* recv, bool allow_sigma) const {
     std::memset(&p, 0, sizeof(p));
     p.n = b_.n;
     p.rank = rank_;
@@ -655,7 +721,14 @@ void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const 
     p.rows4 = reinterpret_cast<const uint4*>(b_.row_ids.p);
     p.L = L_.p;
     p.Vc = V_.p;
-    p.Vn = V_.p + words_ + 4;
+    p.Vn = V_.p + vstride_;
+    if (sigma_built_ && allow_sigma) {
+        p.rows4 = reinterpret_cast<const uint4*>(sigma_.rows.p);
+        p.hot_words = sigma_.hot_words;
+        p.inv = sigma_.inv.p;
+        p.sig = sigma_.sig.p;
+        p.H = H_.p;
+    }
     p.X = xbuf_.p;
     p.peers = peers_.p;
     p.send = send_.p;
@@ -746,8 +819,12 @@ void rows_group_launch(const std::vector<RowsEngine*>& ranks, uint32_t src) {
     const uint32_t cpr = std::min<uint32_t>(g.ctas / G, kAggStride);
     if (cpr < 1) throw InvalidArgument("more virtual ranks than co-resident CTAs");
     std::vector<RowsParams> hp(G);
+    // one grid: every rank must run the same barrier sequence, so the hot-row view (an
+    // extra barrier per level) is used only if every rank has it
+    bool all_sigma = true;
+    for (uint32_t r = 0; r < G; ++r) all_sigma = all_sigma && ranks[r]->sigma_built_;
     for (uint32_t r = 0; r < G; ++r) {
-        ranks[r]->fill_params(hp[r], src, 1, nullptr);
+        ranks[r]->fill_params(hp[r], src, 1, nullptr, all_sigma);
         hp[r].dense_min = rows_dense_min();
         ranks[r]->ctas_ = cpr;
     }

@@ -27,6 +27,7 @@
 
 #include "bvss.cuh"
 #include "common.cuh"
+#include "sigma.cuh"
 
 namespace blestgpu {
 
@@ -73,7 +74,7 @@ public:
     uint32_t world() const { return world_; }
     const DeviceBvss& bvss() const { return b_; }
     // device copy of this rank's kernel parameters (group launch)
-    void fill_params(RowsParams& p, uint32_t src, uint32_t level, const uint32_t* recv) const;
+    void fill_params(RowsParams& p, uint32_t src, uint32_t level, const uint32_t* recv, bool allow_sigma = true) const;
 
 private:
     const DeviceBvss& b_;
@@ -82,7 +83,11 @@ private:
     uint64_t words_, w_lo_, w_hi_, per_, xstride_;
     std::vector<uint64_t> bounds_;
     DevBuf<uint64_t> dbounds_;
-    DevBuf<uint32_t> L_, V_;             // levels (global size), V_curr | V_next (global words + sentinel)
+    DevBuf<uint32_t> L_, V_;             // levels (global size), V_curr | V_next ([hot prefix] + global words + sentinel)
+    uint64_t vstride_ = 0;
+    SigmaView sigma_;                    // hot-row view of the rank's rows (sigma.cuh)
+    bool sigma_built_ = false;
+    DevBuf<uint32_t> H_;                 // hot discoveries of the level, row-space words
     DevBuf<uint32_t> xbuf_;              // exchange: X0 | X1 (xstride each) | arrival counter
     DevBuf<uint32_t> send_;              // stepped: owned diff words (per)
     DevBuf<unsigned long long> q_, sl_, ctl_, agg_, trace_, tstamp_;

@@ -28,6 +28,24 @@ __global__ void k_rank_keys(const uint32_t* __restrict__ cnt, uint32_t n, uint64
         keys[r] = ((uint64_t)(0xFFFFFFFFu - cnt[r]) << 32) | r;
 }
 
+// acc[0] = slots of the first K keys (the hot rows), acc[1] = all slots
+__global__ void k_share(const uint64_t* __restrict__ keys, uint32_t n, uint32_t K, unsigned long long* acc) {
+    unsigned long long hot = 0, all = 0;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long c = 0xFFFFFFFFull - (keys[q] >> 32);
+        all += c;
+        if (q < K) hot += c;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        hot += __shfl_xor_sync(0xffffffffu, hot, o);
+        all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (hot) atomicAdd(&acc[0], hot);
+        if (all) atomicAdd(&acc[1], all);
+    }
+}
+
 __global__ void k_engine_ids(uint32_t n, uint32_t base, uint32_t* __restrict__ sig) {
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
          r += (uint64_t)gridDim.x * blockDim.x)
@@ -79,6 +97,17 @@ void sigma_view_build(const DeviceBvss& b, SigmaView& out, uint32_t hot_cap) {
         CK(cub::DeviceRadixSort::SortKeys(nullptr, temp, keys.p, keys2.p, (int64_t)n, 0, 64, st));
         DevBuf<unsigned char> tmp(temp ? temp : 1);
         CK(cub::DeviceRadixSort::SortKeys(tmp.p, temp, keys.p, keys2.p, (int64_t)n, 0, 64, st));
+        // share of the slots held by the K hot rows (keys2 ascending = most slots first)
+        {
+            DevBuf<unsigned long long> acc(2);
+            CK(cudaMemsetAsync(acc.p, 0, 16, st));
+            k_share<<<grid_for(n, 256), 256, 0, st>>>(keys2.p, n, out.K, acc.p);
+            CK(cudaGetLastError());
+            unsigned long long h[2];
+            CK(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            out.hot_share = h[1] ? (double)h[0] / (double)h[1] : 0.0;
+        }
         k_engine_ids<<<grid_for(n, 256), 256, 0, st>>>(n, (uint32_t)(32 * out.hot_words), out.sig.p);
         if (out.K) k_hot_tables<<<grid_for(out.K, 256), 256, 0, st>>>(keys2.p, out.K, out.sig.p, out.inv.p);
     }

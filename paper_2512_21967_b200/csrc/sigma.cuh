@@ -26,7 +26,13 @@ struct SigmaView {
     DevBuf<uint32_t> rows;   // engine row_ids (hot rank, or 32·hot_words + row); padding kept
     DevBuf<uint32_t> sig;    // row -> engine id
     DevBuf<uint32_t> inv;    // hot rank -> row
+    double hot_share = 0;    // share of the (non-padding) BVSS slots held by the K hot rows
 };
+
+// The view pays off when the hot rows take a large share of the visited tests (Kron-24:
+// ~0.8 of the slots; C2 1.93 -> 1.55 ms); on graphs without hubs (urand-24: ~0.07) its hot
+// pass is pure overhead (C3 2.56 -> 2.60 ms). Engines use it from this share up.
+constexpr double kSigmaMinShare = 0.3;
 
 // hot_cap: most hot rows (0 = default 2^20).
 void sigma_view_build(const DeviceBvss& b, SigmaView& out, uint32_t hot_cap = 0);
