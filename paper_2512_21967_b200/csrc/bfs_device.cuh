@@ -61,7 +61,19 @@ struct Smem {
     unsigned long long ctr[4];                         // discovered, full, relaxed, pushes
     unsigned long long red[THREADS / 32];              // block reductions / scans
     unsigned long long base;
+    unsigned long long nz;                             // stage 2: chunks with a frontier word
 };
+
+// Block-wide OR of a per-thread chunk mask into sm.nz (thread 0 must have zeroed it before a
+// __syncthreads that precedes this call; read it after a later __syncthreads).
+template <int THREADS, int MODE>
+__device__ __forceinline__ void block_or_nz(Smem<THREADS, MODE>& sm, unsigned long long m) {
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)m);
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(m >> 32));
+    if ((threadIdx.x & 31) == 0 && (lo | hi)) atomicOr(&sm.nz, ((unsigned long long)hi << 32) | lo);
+}
+// bit of chunk i (relative to the CTA's first chunk) in the masks; chunks from 63 on share bit 63
+__device__ __forceinline__ unsigned long long chunk_bit(uint64_t i) { return 1ull << (i < 63 ? i : 63); }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
@@ -374,12 +386,14 @@ template <int THREADS>
 __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm, uint32_t level, uint32_t (&ctr)[4],
                                            uint64_t k0, uint64_t k1, bool single, const uint32_t (&keep)[4],
                                            unsigned long long my_vss, unsigned long long my_sets,
-                                           const uint32_t* Fd) {
+                                           const uint32_t* Fd, unsigned long long nzm) {
     constexpr unsigned long long kTagMask = (1ull << 40) - 1;
     constexpr uint64_t CH = 4ull * THREADS;
     // Fd: the frontier words being built this level (parameter)
+    if (threadIdx.x == 0) sm.nz = 0;
     unsigned long long cta = 0;
     block_excl_scan(sm, pack_vs(my_vss, my_sets), &cta);
+    block_or_nz(sm, nzm);
     const unsigned long long cta_vss = cta & kVssMask, cta_sets = cta >> (64 - kSetBits);
     if (threadIdx.x == 0) {
         const unsigned long long tag = (unsigned long long)level << 40;
@@ -405,8 +419,11 @@ __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm
             p.ctl[1] = run_sets + cta_sets;
         }
     }
-    // pass B: SL entries of the CTA's active sets, ascending
+    // pass B: SL entries of the CTA's active sets, ascending; chunks without a frontier
+    // word contribute nothing (no loads, no scans — the skip is uniform over the CTA)
+    const unsigned long long nz = sm.nz;  // after the scans' __syncthreads
     for (uint64_t ch = k0; ch < k1; ++ch) {
+        if (!(nz & chunk_bit(ch - k0))) continue;
         const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
         uint32_t d[4];
         if (single) {
@@ -459,7 +476,7 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
     const uint64_t k0 = (uint64_t)blockIdx.x * chunks / gridDim.x, k1 = (uint64_t)(blockIdx.x + 1) * chunks / gridDim.x;
     const bool single = k1 - k0 <= 1;
     uint32_t keep[4] = {0, 0, 0, 0};  // frontier words of the CTA's only chunk
-    unsigned long long my_vss = 0, my_sets = 0;
+    unsigned long long my_vss = 0, my_sets = 0, nzm = 0;
     // pass A
     for (uint64_t ch = k0; ch < k1; ++ch) {
         const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
@@ -489,6 +506,7 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
                 }
         }
         s2_counts<THREADS>(p, w0, f, my_vss, my_sets);
+        if (f[0] | f[1] | f[2] | f[3]) nzm |= chunk_bit(ch - k0);
         // levels: one coalesced 128 B store per changed word (lane = bit)
         unsigned ball = __ballot_sync(0xffffffffu, any);
         const uint64_t wwarp = ch * CH + 128ull * warp;
@@ -502,7 +520,7 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
             }
         }
     }
-    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets, Fd);
+    s2_enqueue<THREADS>(p, sm, level, ctr, k0, k1, single, keep, my_vss, my_sets, Fd, nzm);
 }
 
 // Hot-row stage 2 (sigma.cuh): the hot prefix of the visited bitmaps (hot_words words,

@@ -48,6 +48,7 @@ struct RowsParams {
     unsigned long long* agg;   // 3 × 4096: per-CTA (level << 40 | VSS), (… | sets), (… | bits)
     unsigned long long* trace;
     unsigned long long* tstamp;  // 4 per level (timeline), may be null
+    uint32_t sys_scope;          // fused exchange with peers on other GPUs (IPC): system-scope sync
     // hot-row view of the rank's rows (sigma.cuh; hot_words = 0: plain row ids): V words =
     // [hot prefix | row words]; inv: hot rank -> row; sig: row -> engine id; H: staging
     // words (row space) for the hot discoveries of the level
@@ -60,7 +61,7 @@ struct RowsParams {
 
 // Every rank's parameters of one launch, passed by value (kernel parameter space: constant
 // bank loads, no per-thread copy of a global struct). One entry per rank of the launch.
-constexpr uint32_t kMaxLaunchRanks = 16;
+constexpr uint32_t kMaxLaunchRanks = 12;
 struct RowsLaunch {
     RowsParams r[kMaxLaunchRanks];
 };
@@ -82,6 +83,14 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // Cross-rank arrival barrier (fused mode). Callers: every thread, after a grid barrier that
 // follows their (system-fenced) peer stores. Thread 0 of the rank's first CTA adds 1 to every
@@ -93,13 +102,22 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 __device__ bool cross_rank_barrier(const RowsParams& p, uint32_t vb) {
     volatile unsigned* abort_word = p.X + 2 * p.xstride + 1;
     if (vb == 0 && threadIdx.x == 0) {
-        for (uint32_t r = 0; r < p.world; ++r)
-            red_release_sys_add(reinterpret_cast<unsigned*>(p.peers[r]) + 2 * p.xstride, 1u);
+        // peers on other GPUs (IPC mappings): system scope; virtual ranks of one device share
+        // its L2, so device scope suffices (a system-scope release costs ~0.3 ms per level here)
+        if (p.sys_scope) {
+            __threadfence_system();  // cumulative: every CTA's stores ordered before it by the grid barrier
+            for (uint32_t r = 0; r < p.world; ++r)
+                red_release_sys_add(reinterpret_cast<unsigned*>(p.peers[r]) + 2 * p.xstride, 1u);
+        } else {
+            for (uint32_t r = 0; r < p.world; ++r)
+                red_release_gpu_add(reinterpret_cast<unsigned*>(p.peers[r]) + 2 * p.xstride, 1u);
+        }
         const unsigned* mine = p.X + 2 * p.xstride;
         const unsigned long long passed = p.ctl[kXBar];
         const unsigned want = (unsigned)(p.world * (passed + 1));
         const unsigned long long t0 = globaltimer();
-        while (!*abort_word && (int)(ld_acquire_sys(mine) - want) < 0) {
+        while (!*abort_word &&
+               (int)((p.sys_scope ? ld_acquire_sys(mine) : ld_acquire_gpu_u32(mine)) - want) < 0) {
             if (globaltimer() - t0 > kTimeoutNs) {
                 p.ctl[kStatus] = 2;
                 for (uint32_t r = 0; r < p.world; ++r)
@@ -131,8 +149,8 @@ __device__ __forceinline__ uint32_t gathered_word(const RowsParams& p, uint64_t 
 // (set | first position << 32) in ascending order: per-CTA counts published with a level
 // tag, predecessors summed, no contended atomics. The rank's last CTA stores the totals.
 template <int THREADS, bool STEPPED>
-__device__ void stage2b(const RowsParams& p, Smem<THREADS, 1>& sm, uint32_t level, uint32_t vb, uint32_t vG,
-                        const uint32_t* Xsrc, uint32_t (&ctr)[4]) {
+__device__ unsigned long long stage2b(const RowsParams& p, Smem<THREADS, 1>& sm, uint32_t level, uint32_t vb,
+                                      uint32_t vG, const uint32_t* Xsrc, uint32_t (&ctr)[4]) {
     constexpr uint64_t CH = 4ull * THREADS;
     const uint64_t chunks = (p.words + CH - 1) / CH;
     const uint64_t k0 = (uint64_t)vb * chunks / vG, k1 = (uint64_t)(vb + 1) * chunks / vG;
@@ -165,17 +183,20 @@ __device__ void stage2b(const RowsParams& p, Smem<THREADS, 1>& sm, uint32_t leve
                     ns += c != 0;
                 }
     };
-    unsigned long long my_v = 0, my_s = 0, my_b = 0;
+    unsigned long long my_v = 0, my_s = 0, my_b = 0, nzm = 0;
+    if (threadIdx.x == 0) sm.nz = 0;
     for (uint64_t ch = k0; ch < k1; ++ch) {
         const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
         uint32_t d[4];
         load4(w0, d, true);
 #pragma unroll
         for (int k = 0; k < 4; ++k) my_b += __popc(d[k]);
+        if (d[0] | d[1] | d[2] | d[3]) nzm |= chunk_bit(ch - k0);
         counts(w0, d, my_v, my_s);
     }
     unsigned long long cta_v = 0, cta_s = 0, cta_b = 0;
     block_excl_scan(sm, my_v, &cta_v);
+    block_or_nz(sm, nzm);
     block_excl_scan(sm, my_s, &cta_s);
     block_excl_scan(sm, my_b, &cta_b);
     unsigned long long* aggV = p.agg;
@@ -219,7 +240,9 @@ __device__ void stage2b(const RowsParams& p, Smem<THREADS, 1>& sm, uint32_t leve
         }
     }
     const uint32_t* Xs = STEPPED ? X0 : Xsrc;
+    const unsigned long long nz = sm.nz;  // after the scans' __syncthreads
     for (uint64_t ch = k0; ch < k1; ++ch) {
+        if (!(nz & chunk_bit(ch - k0))) continue;  // no frontier word: nothing to queue
         const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
         uint32_t d[4];
 #pragma unroll
@@ -246,6 +269,7 @@ __device__ void stage2b(const RowsParams& p, Smem<THREADS, 1>& sm, uint32_t leve
         run_v += it_v;
         run_s += it_s;
     }
+    return nz;  // the CTA's chunks holding a frontier word (clear list of the next level)
 }
 
 // Stage 2a: the owned V words — diff = V_next & ~V_curr, V_curr = V_next, levels (one
@@ -421,6 +445,15 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
         }
     }
 
+    // fused: the CTA's 2b chunks holding the last frontier's words (level 1: the source's)
+    unsigned long long prev_nz = 0;
+    {
+        constexpr uint64_t CH = 4ull * THREADS;
+        const uint64_t chunks = (p.words + CH - 1) / CH;
+        const uint64_t k0 = (uint64_t)vb * chunks / vG, k1 = (uint64_t)(vb + 1) * chunks / vG;
+        const uint64_t cs = (uint64_t)(p.src >> 5) / CH;
+        if (cs >= k0 && cs < k1) prev_nz = chunk_bit(cs - k0);
+    }
     for (;; ++level) {
         const unsigned long long len = ld_relaxed_gpu_u64(&p.ctl[kT]);
         const uint32_t S = (uint32_t)ld_relaxed_gpu_u64(&p.ctl[kS]);
@@ -494,22 +527,35 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
             return;  // host: all-gather, then the next level's launch
         }
         const uint64_t xo = (uint64_t)(level & 1) * p.xstride;
-        bool stored = false;
         stage2a(p, level, gtid, gthreads, ctr, [&](uint64_t w, uint32_t d) {
-            if (d) {
+            if (d)
                 for (uint32_t r = 0; r < p.world; ++r) reinterpret_cast<uint32_t*>(p.peers[r])[xo + w] = d;
-                stored = true;
-            }
         });
-        uint32_t* Fold = p.X + ((level - 1) & 1) * p.xstride;  // this level's α: read by stage 1 only
-        for (uint64_t w = gtid; w < p.words; w += gthreads) Fold[w] = 0;
-        if (stored) __threadfence_system();
+        // this level's α words (read by stage 1 only) are cleared for the level after next:
+        // only the CTA's 2b chunks that held a frontier word (prev_nz, from the last 2b)
+        {
+            uint32_t* Fold = p.X + ((level - 1) & 1) * p.xstride;
+            constexpr uint64_t CH = 4ull * THREADS;
+            const uint64_t chunks = (p.words + CH - 1) / CH;
+            const uint64_t k0 = (uint64_t)vb * chunks / vG, k1 = (uint64_t)(vb + 1) * chunks / vG;
+            for (uint64_t ch = k0; ch < k1; ++ch) {
+                if (!(prev_nz & chunk_bit(ch - k0))) continue;
+                const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
+                if (w0 + 4 <= p.words) {
+                    *reinterpret_cast<uint4*>(Fold + w0) = make_uint4(0, 0, 0, 0);
+                } else {
+                    for (uint64_t w = w0; w < p.words && w < w0 + 4; ++w) Fold[w] = 0;
+                }
+            }
+        }
+        // the peer stores are ordered before the arrival by this grid barrier (gpu scope) and
+        // the cumulative system-scope fence + release of cross_rank_barrier's thread
         grid_sync();
         if (!cross_rank_barrier(p, vb)) break;
         stamp(p, vb, level, 2);
 
         // ---- stage 2b: the whole exchanged frontier → termination, next SL ----
-        stage2b<THREADS, false>(p, sm, level, vb, vG, p.X + xo, ctr);
+        prev_nz = stage2b<THREADS, false>(p, sm, level, vb, vG, p.X + xo, ctr);
         grid_sync();
         trace_add<THREADS>(p, sm, level, ctr);
         stamp(p, vb, level, 3);
@@ -741,6 +787,7 @@ void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const 
     p.trace = trace_.p;
     p.tstamp = tstamp_.p;
     p.hflags = hflags_dev_;
+    p.sys_scope = opened_.empty() ? 0u : 1u;
 }
 
 namespace {
@@ -811,7 +858,7 @@ void RowsEngine::step(uint32_t level, uint32_t src, const uint32_t* recv) {
 void rows_group_launch(const std::vector<RowsEngine*>& ranks, uint32_t src) {
     const uint32_t G = (uint32_t)ranks.size();
     if (!G) throw InvalidArgument("empty rank group");
-    if (G > kMaxLaunchRanks) throw InvalidArgument("at most 16 virtual ranks per launch");
+    if (G > kMaxLaunchRanks) throw InvalidArgument("at most 12 virtual ranks per launch");
     for (uint32_t r = 0; r < G; ++r)
         if (ranks[r]->rank_ != r || ranks[r]->world_ != G) throw InvalidArgument("rank group out of order");
     if (src >= ranks[0]->b_.n) throw InvalidArgument("bfs source out of range");
