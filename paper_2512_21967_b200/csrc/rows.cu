@@ -49,6 +49,7 @@ struct RowsParams {
     unsigned long long* trace;
     unsigned long long* tstamp;  // 4 per level (timeline), may be null
     uint32_t sys_scope;          // fused exchange with peers on other GPUs (IPC): system-scope sync
+    uint32_t xstamp;             // timing study (BLEST_XFLAGS): exchange-phase stamp point, 0 = default
     // hot-row view of the rank's rows (sigma.cuh; hot_words = 0: plain row ids): V words =
     // [hot prefix | row words]; inv: hot rank -> row; sig: row -> engine id; H: staging
     // words (row space) for the hot discoveries of the level
@@ -185,14 +186,42 @@ __device__ unsigned long long stage2b(const RowsParams& p, Smem<THREADS, 1>& sm,
     };
     unsigned long long my_v = 0, my_s = 0, my_b = 0, nzm = 0;
     if (threadIdx.x == 0) sm.nz = 0;
-    for (uint64_t ch = k0; ch < k1; ++ch) {
-        const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
-        uint32_t d[4];
-        load4(w0, d, true);
+    if (STEPPED) {
+        for (uint64_t ch = k0; ch < k1; ++ch) {
+            const uint64_t w0 = ch * CH + 4ull * threadIdx.x;
+            uint32_t d[4];
+            load4(w0, d, true);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) my_b += __popc(d[k]);
-        if (d[0] | d[1] | d[2] | d[3]) nzm |= chunk_bit(ch - k0);
-        counts(w0, d, my_v, my_s);
+            for (int k = 0; k < 4; ++k) my_b += __popc(d[k]);
+            if (d[0] | d[1] | d[2] | d[3]) nzm |= chunk_bit(ch - k0);
+            counts(w0, d, my_v, my_s);
+        }
+    } else {
+        // fused: 4 chunks per round, their uint4 loads issued together (X is 16-byte aligned)
+        constexpr int U = 4;
+        for (uint64_t c0 = k0; c0 < k1; c0 += U) {
+            uint32_t d[U][4];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t w0 = (c0 + u) * CH + 4ull * threadIdx.x;
+                if (c0 + u < k1 && w0 + 4 <= p.words) {
+                    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(Xsrc + w0));
+                    d[u][0] = v.x; d[u][1] = v.y; d[u][2] = v.z; d[u][3] = v.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) d[u][k] = (c0 + u < k1 && w0 + k < p.words) ? __ldcg(Xsrc + w0 + k) : 0u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (c0 + u >= k1) break;
+                const uint64_t w0 = (c0 + u) * CH + 4ull * threadIdx.x;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) my_b += __popc(d[u][k]);
+                if (d[u][0] | d[u][1] | d[u][2] | d[u][3]) nzm |= chunk_bit(c0 + u - k0);
+                counts(w0, d[u], my_v, my_s);
+            }
+        }
     }
     unsigned long long cta_v = 0, cta_s = 0, cta_b = 0;
     block_excl_scan(sm, my_v, &cta_v);
@@ -277,32 +306,42 @@ __device__ unsigned long long stage2b(const RowsParams& p, Smem<THREADS, 1>& sm,
 template <typename Emit>
 __device__ __forceinline__ void stage2a(const RowsParams& p, uint32_t level, uint64_t gtid, uint64_t gthreads,
                                         uint32_t (&ctr)[4], Emit emit) {
+    constexpr int U = 4;  // words per thread per round, their loads issued together
     const unsigned lane = lane_id();
     const uint64_t span = p.w_hi - p.w_lo;
     uint32_t* Vc = p.Vc + p.hot_words;  // row words (after the hot prefix)
     const uint32_t* Vn = p.Vn + p.hot_words;
-    for (uint64_t i0 = gtid - lane; i0 < span; i0 += gthreads) {
-        const uint64_t w = p.w_lo + i0 + lane;
-        uint32_t d = 0, out = 0;
-        if (i0 + lane < span) {
-            const uint32_t nx = __ldcg(Vn + w);
-            d = nx & ~Vc[w];
-            if (d) Vc[w] = nx;
-            out = d;
-            if (p.hot_words) {  // the hot rows' discoveries (levels already stored)
-                out |= __ldcg(p.H + w);
-                p.H[w] = 0u;
-            }
-            emit(w, out);
+    const bool hot = p.hot_words != 0;
+    for (uint64_t i0 = gtid - lane; i0 < span; i0 += U * gthreads) {
+        uint32_t nx[U], cu[U], h[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + u * gthreads + lane;
+            const uint64_t w = p.w_lo + i;
+            const bool ok = i < span;
+            nx[u] = ok ? __ldcg(Vn + w) : 0u;
+            cu[u] = ok ? Vc[w] : 0u;
+            h[u] = (ok && hot) ? __ldcg(p.H + w) : 0u;  // the hot rows' discoveries (levels stored)
         }
-        ctr[0] += __popc(d);
-        unsigned ball = __ballot_sync(0xffffffffu, d != 0);
-        while (ball) {
-            const int k = __ffs(ball) - 1;
-            ball &= ball - 1;
-            const uint32_t dk = __shfl_sync(0xffffffffu, d, k);
-            const uint64_t wk = p.w_lo + i0 + k;
-            if ((dk >> lane) & 1u) p.L[32 * wk + lane] = level;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t iw = i0 + u * gthreads;  // the warp's first word of this round
+            const uint64_t w = p.w_lo + iw + lane;
+            const uint32_t d = nx[u] & ~cu[u];
+            if (iw + lane < span) {
+                if (d) Vc[w] = nx[u];
+                if (hot && h[u]) p.H[w] = 0u;
+                emit(w, d | h[u]);
+            }
+            ctr[0] += __popc(d);
+            unsigned ball = __ballot_sync(0xffffffffu, d != 0);
+            while (ball) {
+                const int k = __ffs(ball) - 1;
+                ball &= ball - 1;
+                const uint32_t dk = __shfl_sync(0xffffffffu, d, k);
+                const uint64_t wk = p.w_lo + iw + k;
+                if ((dk >> lane) & 1u) p.L[32 * wk + lane] = level;
+            }
         }
     }
 }
@@ -520,6 +559,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
         if (p.hot_words) {  // same on every rank of a launch: the barrier counts match
             stage2a_hot(p, level, vb, vG, ctr);
             grid_sync();
+            if (p.xstamp == 1) stamp(p, vb, level, 2);
         }
         if (STEPPED) {
             stage2a(p, level, gtid, gthreads, ctr, [&](uint64_t w, uint32_t d) { p.send[w - p.w_lo] = d; });
@@ -531,6 +571,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
             if (d)
                 for (uint32_t r = 0; r < p.world; ++r) reinterpret_cast<uint32_t*>(p.peers[r])[xo + w] = d;
         });
+        if (p.xstamp == 2) stamp(p, vb, level, 2);
         // this level's α words (read by stage 1 only) are cleared for the level after next:
         // only the CTA's 2b chunks that held a frontier word (prev_nz, from the last 2b)
         {
@@ -551,8 +592,9 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
         // the peer stores are ordered before the arrival by this grid barrier (gpu scope) and
         // the cumulative system-scope fence + release of cross_rank_barrier's thread
         grid_sync();
+        if (p.xstamp == 3) stamp(p, vb, level, 2);
         if (!cross_rank_barrier(p, vb)) break;
-        stamp(p, vb, level, 2);
+        if (p.xstamp == 0) stamp(p, vb, level, 2);
 
         // ---- stage 2b: the whole exchanged frontier → termination, next SL ----
         prev_nz = stage2b<THREADS, false>(p, sm, level, vb, vG, p.X + xo, ctr);
@@ -788,6 +830,7 @@ void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const 
     p.tstamp = tstamp_.p;
     p.hflags = hflags_dev_;
     p.sys_scope = opened_.empty() ? 0u : 1u;
+    if (const char* x = getenv("BLEST_XSTAMP")) p.xstamp = (uint32_t)atoi(x);
 }
 
 namespace {
