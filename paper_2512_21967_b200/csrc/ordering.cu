@@ -1,15 +1,23 @@
-// Orderings, host side: the classifier's fit, random order and source sampling (the
-// reference's Rng stream). RCM (rcm.cu) and Jaccard windows (jaccard.cu) run on the GPU.
+// Orderings: the classifier (degree histogram on the GPU, the log-log fit on the host in the
+// reference's operation order), random order and source sampling (the reference's Rng
+// stream). RCM (rcm.cu) and Jaccard windows (jaccard.cu) run on the GPU.
 #include <algorithm>
 #include <cmath>
 #include <map>
 #include <random>
+
+#include <cub/cub.cuh>
 
 #include "ordering.cuh"
 
 namespace blestgpu {
 
 namespace {
+
+__global__ void k_out_degrees(const uint64_t* __restrict__ off, uint32_t n, uint64_t* __restrict__ deg) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x)
+        deg[u] = off[u + 1] - off[u];
+}
 
 // Rng (R:include/blest/rng.hpp:11-36): std::mt19937_64's raw stream is fixed by the
 // standard; next_below is the reference's explicit rejection sampler.
@@ -32,15 +40,34 @@ SocialReport classify_social_like(const DeviceGraph& g) {
     SocialReport rep;
     const uint32_t n = g.n;
     if (n == 0) return rep;
-    std::vector<uint64_t> off((size_t)n + 1);
-    CK(cudaMemcpyAsync(off.data(), g.off.p, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost, stream()));
-    CK(cudaStreamSynchronize(stream()));
-    std::map<uint64_t, uint32_t> histogram;  // degree -> #vertices (R:src/ordering.cpp:357-362)
-    uint64_t total = 0;
-    for (uint32_t u = 0; u < n; ++u) {
-        const uint64_t d = off[u + 1] - off[u];
-        ++histogram[d];
-        total += d;
+    // degree histogram (R:src/ordering.cpp:357-362) on the device: out-degrees, radix sort,
+    // run-length encode; only the (degree, #vertices) pairs come to the host for the fit
+    std::map<uint64_t, uint32_t> histogram;  // degree -> #vertices
+    const uint64_t total = g.m;               // Σ out-degrees
+    {
+        cudaStream_t st = stream();
+        DevBuf<uint64_t> deg(n), sorted(n), uniq(n);
+        DevBuf<uint32_t> cnt(n);
+        DevBuf<uint32_t> nrun(1);
+        k_out_degrees<<<grid_for(n, 256), 256, 0, st>>>(g.off.p, n, deg.p);
+        CK(cudaGetLastError());
+        size_t t1 = 0, t2 = 0;
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, t1, deg.p, sorted.p, (int64_t)n, 0, 64, st));
+        CK(cub::DeviceRunLengthEncode::Encode(nullptr, t2, sorted.p, uniq.p, cnt.p, nrun.p, (int64_t)n, st));
+        DevBuf<unsigned char> tmp(std::max<size_t>({t1, t2, 1}));
+        CK(cub::DeviceRadixSort::SortKeys(tmp.p, t1, deg.p, sorted.p, (int64_t)n, 0, 64, st));
+        CK(cub::DeviceRunLengthEncode::Encode(tmp.p, t2, sorted.p, uniq.p, cnt.p, nrun.p, (int64_t)n, st));
+        uint32_t runs = 0;
+        CK(cudaMemcpyAsync(&runs, nrun.p, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<uint64_t> hd(runs);
+        std::vector<uint32_t> hc(runs);
+        if (runs) {
+            CK(cudaMemcpyAsync(hd.data(), uniq.p, runs * 8ull, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(hc.data(), cnt.p, runs * 4ull, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        for (uint32_t i = 0; i < runs; ++i) histogram.emplace_hint(histogram.end(), hd[i], hc[i]);
     }
     if (total == 0) return rep;
     // share(percent) (:367-373): top floor(n*p/100 + 1e-9) degrees (clamped to [1, n]),
