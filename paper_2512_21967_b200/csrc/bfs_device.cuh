@@ -506,16 +506,18 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
                 }
         }
         s2_counts<THREADS>(p, w0, f, my_vss, my_sets);
-        if (f[0] | f[1] | f[2] | f[3]) nzm |= chunk_bit(ch - k0);
-        // levels: one coalesced 128 B store per changed word (lane = bit)
-        unsigned ball = __ballot_sync(0xffffffffu, any);
+        const bool fany = (f[0] | f[1] | f[2] | f[3]) != 0u;
+        if (fany) nzm |= chunk_bit(ch - k0);
+        // levels of every discovery of the word — cold (d) and, with the hot view, the hot
+        // rows merged into f: one coalesced 128 B store per changed word (lane = bit)
+        unsigned ball = __ballot_sync(0xffffffffu, HOT ? fany : any);
         const uint64_t wwarp = ch * CH + 128ull * warp;
         while (ball) {
             const int src = __ffs(ball) - 1;
             ball &= ball - 1;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t dk = __shfl_sync(0xffffffffu, d[k], src);
+                const uint32_t dk = __shfl_sync(0xffffffffu, HOT ? f[k] : d[k], src);
                 if ((dk >> lane) & 1u) p.L[32 * (wwarp + 4 * src + k) + lane] = level;
             }
         }
@@ -524,9 +526,10 @@ __device__ __forceinline__ void lazy_stage2(const Params& p, Smem<THREADS, 1>& s
 }
 
 // Hot-row stage 2 (sigma.cuh): the hot prefix of the visited bitmaps (hot_words words,
-// one per thread) — diff, V_curr update, and each hot discovery mapped back (σ⁻¹) to store
-// its level and RED its bit into the original-space frontier Fd (zeroed during stage 1);
-// a grid barrier; then lazy_stage2<HOT> sweeps the row words and merges Fd.
+// one per thread) — diff, V_curr update, and each hot discovery mapped back (σ⁻¹) to RED
+// its bit into the original-space frontier Fd (zeroed during stage 1); a grid barrier;
+// then lazy_stage2<HOT> sweeps the row words, merges Fd and writes the levels of both
+// (coalesced, instead of one scattered store per hot discovery).
 template <int THREADS>
 __device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1>& sm, uint32_t level,
                                                 uint32_t (&ctr)[4], unsigned& gen, uint32_t* Fd) {
@@ -554,10 +557,7 @@ __device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1
             }
 #pragma unroll
             for (int t = 0; t < 8; ++t)
-                if ((bits >> t) & 1u) {
-                    p.L[rr[t]] = level;
-                    red_or(Fd + (rr[t] >> 5), 1u << (rr[t] & 31));
-                }
+                if ((bits >> t) & 1u) red_or(Fd + (rr[t] >> 5), 1u << (rr[t] & 31));  // level: row sweep
         }
     }
     grid_barrier(p.bar, gen);  // the hot discoveries are in Fd
