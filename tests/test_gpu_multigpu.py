@@ -200,3 +200,63 @@ def test_gloo_world2_drives_gpu_engines(oracle, tmp_path):
         assert np.array_equal(got, want), f
         cnt = z["cnt"]
         assert (cnt[:, 0] == cnt[0, 0]).all() and cnt[0, 0] == cnt[0, 1] + 1 + 2
+
+
+def _ipc_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(HERE))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_2512_21967_b200 as Bw
+    from paper_2512_21967_b200 import _lib as Lw
+    from paper_2512_21967_b200.multigpu import RowsEngine as RE, exchange_ipc_handles, partition_rows as pr
+    Lw.check(Lw.lib().blest_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    g = Bw.Graph.generate_rmat(10, 8, 3)
+    n = g.num_vertices()
+    bounds, _ = pr(g, world)
+    eng = RE(g, rank, world, bounds)
+    exchange_ipc_handles(eng)  # CUDA IPC mappings of the peers' frontier buffers
+    for k, src in enumerate(g.pick_sources(2, 5)):
+        dist.barrier()
+        eng.bfs(int(src))  # fused: peer stores + in-kernel cross-rank barrier (system scope)
+        r = eng.finish()
+        mine = torch.full((32 * eng.per,), -1, dtype=torch.int64)
+        mine[: r.row_hi - r.row_lo] = torch.from_numpy(r.levels.astype(np.int64))
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        if rank == 0:
+            got = np.concatenate([p.numpy()[: min(32 * bounds[i + 1], n) - min(32 * bounds[i], n)]
+                                  for i, p in enumerate(parts)])
+            off, tgt = g.csr()
+            np.savez(os.path.join(out_dir, f"s{k}.npz"), got=got, src=int(src), off=off, tgt=tgt)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(os.environ.get("BLEST_TEST_IPC") != "1",
+                    reason="opt-in (BLEST_TEST_IPC=1): two processes time-share one GPU, each fused "
+                           "kernel waiting for the other at every level")
+def test_ipc_fused_two_processes(oracle, tmp_path):
+    """The fused P2P mode across two real processes: CUDA IPC handles exchanged over
+    torch.distributed, frontier words stored into the peer's buffer, system-scope arrival
+    barrier. On one GPU the two cooperative kernels time-slice, so each level waits for a
+    context switch — a functional test of the multi-GPU plumbing, not a timing."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_ipc_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    files = sorted(os.listdir(tmp_path))
+    assert len(files) == 2
+    for f in files:
+        z = np.load(os.path.join(tmp_path, f))
+        got = z["got"].astype(np.int64)
+        off, tgt = z["off"], z["tgt"]
+        want = oracle.reference_bfs(oracle.Csr(len(off) - 1, off, tgt), int(z["src"]))[0].astype(np.int64)
+        got[got == 0xFFFFFFFF] = -1
+        want[want == 0xFFFFFFFF] = -1
+        assert np.array_equal(got, want), f
