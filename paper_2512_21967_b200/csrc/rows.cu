@@ -49,7 +49,7 @@ struct RowsParams {
     unsigned long long* trace;
     unsigned long long* tstamp;  // 4 per level (timeline), may be null
     uint32_t sys_scope;          // fused exchange with peers on other GPUs (IPC): system-scope sync
-    uint32_t xstamp;             // timing study (BLEST_XFLAGS): exchange-phase stamp point, 0 = default
+    uint32_t xstamp;             // timing study (BLEST_XSTAMP): exchange-phase stamp point, 0 = default
     // hot-row view of the rank's rows (sigma.cuh; hot_words = 0: plain row ids): V words =
     // [hot prefix | row words]; inv: hot rank -> row; sig: row -> engine id; H: staging
     // words (row space) for the hot discoveries of the level

@@ -16,5 +16,5 @@ BLEST_DIST_BACKEND=gloo timeout 1200 python -m torch.distributed.run --nnodes=1 
 timeout 900 python tools/rows_profile.py --config c5 --ranks 8 --sources 1 > gpurun_out/final/rows_prof_c5_8.json 2> gpurun_out/final/rows_prof_c5_8.err
 timeout 600 python tools/phase_profile.py --config c2 --sources 2 > gpurun_out/final/phase_c2.txt 2>&1
 timeout 600 python tools/phase_profile.py --config c3 --sources 1 > gpurun_out/final/phase_c3.txt 2>&1
-timeout 1500 bash tools/profile.sh c3 > gpurun_out/final/profile_c3.log 2>&1
+timeout 1500 bash tools/profile.sh c2 > gpurun_out/final/profile_c2.log 2>&1
 ls -la gpurun_out/final
