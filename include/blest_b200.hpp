@@ -24,7 +24,10 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
+#include <functional>
+#include <thread>
 #include <limits>
 #include <map>
 #include <memory>
@@ -634,6 +637,138 @@ inline AutoResult run_auto(const Graph& g, VertexId src, const AutoConfig& cfg) 
                                                                        : "identity";
     b.producing_permutation = std::move(perm);
     return run_auto_prebuilt(b, plan, src, cfg);
+}
+
+// ---- row-partitioned multi-GPU BFS (no reference counterpart: SURVEY §8(e); the C-ABI
+// blest_partition_rows / blest_rows_*, paper_2512_21967_b200/multigpu.py is the Python twin)
+class RowsEngine {
+public:
+    // Slice-balanced frontier-word bounds (world + 1 entries); slices per rank optional.
+    static std::vector<std::uint64_t> partition(const Graph& g, std::uint32_t world,
+                                                std::vector<std::uint64_t>* slices = nullptr) {
+        std::vector<std::uint64_t> b(world + 1), sl(world);
+        detail::check(blest_partition_rows(g.handle(), world, b.data(), sl.data()));
+        if (slices) *slices = sl;
+        return b;
+    }
+    RowsEngine(const Graph& g, std::uint32_t rank, std::uint32_t world, const std::vector<std::uint64_t>& bounds)
+        : world_(world) {
+        if (bounds.size() != (std::size_t)world + 1) throw std::invalid_argument("world + 1 word bounds expected");
+        blest_rows h = nullptr;
+        detail::check(blest_rows_create(g.handle(), rank, world, bounds.data(), &h));
+        h_.reset(h);
+        std::uint32_t lo = 0, hi = 0, nv = 0;
+        std::uint64_t per = 0;
+        detail::check(blest_rows_info(h, &lo, &hi, &nv, &per));
+        row_lo_ = lo;
+        row_hi_ = hi;
+        num_vss_ = nv;
+        per_ = per;
+    }
+    VertexId row_lo() const { return row_lo_; }
+    VertexId row_hi() const { return row_hi_; }
+    std::uint32_t num_vss() const { return num_vss_; }
+    std::uint64_t per_words() const { return per_; }
+    std::uint32_t world() const { return world_; }
+    blest_rows handle() const { return h_.get(); }
+
+    // fused (P2P) mode: CUDA IPC handle of the frontier buffer; every rank's, rank-major
+    std::array<char, 64> ipc_handle() const {
+        std::array<char, 64> a{};
+        detail::check(blest_rows_ipc_handle(h_.get(), a.data()));
+        return a;
+    }
+    void open_peers(const std::vector<std::array<char, 64>>& handles) {
+        std::vector<char> blob;
+        for (const auto& a : handles) blob.insert(blob.end(), a.begin(), a.end());
+        detail::check(blest_rows_open_peers(h_.get(), blob.data()));
+    }
+    void bfs(VertexId src) { detail::check(blest_rows_bfs(h_.get(), src)); }
+
+    // stepped (NCCL) mode
+    std::uint32_t* send_buffer() const {
+        std::uint32_t* p = nullptr;
+        detail::check(blest_rows_send_buffer(h_.get(), &p));
+        return p;
+    }
+    void step(std::uint32_t level, VertexId src, const std::uint32_t* recv_device) {
+        detail::check(blest_rows_step(h_.get(), level, src, recv_device));
+    }
+    void flags(std::uint32_t& progress, std::uint32_t& done, std::uint32_t& status) const {
+        detail::check(blest_rows_flags(h_.get(), &progress, &done, &status));
+    }
+
+    // the owned rows' levels [row_lo, row_hi) and the per-BFS counters
+    std::vector<Level> finish(blest_rows_stats* stats = nullptr) {
+        std::vector<Level> lv(row_hi_ - row_lo_);
+        blest_rows_stats st{};
+        detail::check(blest_rows_finish(h_.get(), lv.data(), &st));
+        if (stats) *stats = st;
+        return lv;
+    }
+
+private:
+    struct Del {
+        void operator()(blest_rows_s* r) const { blest_rows_free(r); }
+    };
+    std::unique_ptr<blest_rows_s, Del> h_;
+    std::uint32_t world_ = 0, num_vss_ = 0;
+    VertexId row_lo_ = 0, row_hi_ = 0;
+    std::uint64_t per_ = 0;
+};
+
+// The stepped-mode host protocol (one rank; multigpu.SteppedBfs): level 1 from src, then per
+// level the caller's all-gather of send_buffer() (per_words u32 per rank) into recv_device
+// (world × per_words u32, rank-major) — e.g. ncclAllGather on the library's stream — and the
+// next launch, never waiting for a level: the kernels' mapped flags give termination, the
+// host runs at most `ahead` levels in front, and every rank issues iterations + 1 + ahead
+// all-gathers (so collectives match across ranks). max_levels > 0 caps the launches.
+struct RowsOutcome {
+    std::vector<Level> levels;  // owned rows [row_lo, row_hi)
+    blest_rows_stats stats{};
+    std::uint32_t collectives = 0;
+};
+inline RowsOutcome rows_bfs_stepped(RowsEngine& e, VertexId src, std::uint32_t* recv_device,
+                                    const std::function<void(const std::uint32_t*, std::uint32_t*, std::uint64_t)>& allgather,
+                                    std::uint32_t ahead = 2, std::uint32_t max_levels = 0) {
+    e.step(1, src, nullptr);
+    std::uint32_t issued = 0, done = 0;
+    std::int64_t target = -1;
+    while (target < 0 || (std::int64_t)issued < target) {
+        for (;;) {  // run-ahead limit: the launch issued + 1 - ahead has started
+            std::uint32_t prog = 0, d = 0, status = 0;
+            e.flags(prog, d, status);
+            if (d && target < 0) {
+                done = d;
+                target = (std::int64_t)done + 1 + ahead;  // identical on every rank
+            }
+            if ((std::int64_t)prog + ahead >= (std::int64_t)issued + 1 || target >= 0) break;
+            std::this_thread::yield();
+        }
+        if (target >= 0 && (std::int64_t)issued >= target) break;
+        if (max_levels && issued >= max_levels)
+            throw std::runtime_error("BFS ran past the level safety cap at level " + std::to_string(issued + 1));
+        allgather(e.send_buffer(), recv_device, e.per_words());
+        ++issued;
+        e.step(issued + 1, src, recv_device);
+    }
+    RowsOutcome out;
+    out.levels = e.finish(&out.stats);
+    out.collectives = issued;
+    if (out.stats.iterations != done) throw std::logic_error("ranks' termination level disagrees with the engine");
+    return out;
+}
+
+// Virtual ranks: every engine of this device in one fused launch (peers = the siblings).
+inline void rows_set_local_peers(const std::vector<RowsEngine*>& ranks) {
+    std::vector<blest_rows> h;
+    for (auto* r : ranks) h.push_back(r->handle());
+    detail::check(blest_rows_set_local_peers(h.data(), (std::uint32_t)h.size()));
+}
+inline void rows_group_bfs(const std::vector<RowsEngine*>& ranks, VertexId src) {
+    std::vector<blest_rows> h;
+    for (auto* r : ranks) h.push_back(r->handle());
+    detail::check(blest_rows_group_bfs(h.data(), (std::uint32_t)h.size(), src));
 }
 
 }  // namespace blest

@@ -5,10 +5,13 @@
 // oracle/ref_shim.cpp — test infrastructure, linked only into this test program).
 #include <cstdio>
 #include <unistd.h>
+#include <barrier>
 #include <fstream>
 #include <random>
 #include <stdexcept>
 #include <string>
+
+#include <cuda_runtime.h>
 
 #include "blest_b200.hpp"
 
@@ -118,6 +121,74 @@ int main() {
                         CHECK(c.mma_calls == 2 * c.vss_dequeues);
                     }
             }
+        }
+    }
+    // row-partitioned engine (blest_rows_*, include/blest_b200.hpp RowsEngine): the assembled
+    // owned levels equal the reference's reference_bfs — virtual ranks in one fused launch,
+    // and the stepped host protocol (rows_bfs_stepped) on one rank per host thread with a
+    // device all-gather standing in for ncclAllGather
+    for (bool directed : {false, true}) {
+        std::mt19937_64 rng(23 + directed);
+        const VertexId n = 7000;
+        std::vector<std::pair<VertexId, VertexId>> e;
+        for (int i = 0; i < 8 * (int)n; ++i) e.emplace_back(rng() % n, rng() % n);
+        const Graph g = Graph::from_edges(n, e, directed);
+        const RefGraph rg(n, e, directed);
+        const VertexId srcs[] = {0, n / 3, n - 1};
+        for (std::uint32_t world : {1u, 2u, 3u}) {
+            std::vector<std::uint64_t> slices;
+            const auto bounds = RowsEngine::partition(g, world, &slices);
+            CHECK(bounds.size() == world + 1 && bounds.front() == 0 && bounds.back() == (n + 31) / 32);
+            auto make = [&] {
+                std::vector<std::unique_ptr<RowsEngine>> r;
+                for (std::uint32_t k = 0; k < world; ++k) r.push_back(std::make_unique<RowsEngine>(g, k, world, bounds));
+                return r;
+            };
+            // fused: G virtual ranks of this device, one launch per BFS
+            auto ranks = make();
+            std::vector<RowsEngine*> ptrs;
+            for (auto& r : ranks) ptrs.push_back(r.get());
+            rows_set_local_peers(ptrs);
+            for (VertexId s : srcs) {
+                rows_group_bfs(ptrs, s);
+                std::vector<Level> L(n, 0);
+                for (std::uint32_t k = 0; k < world; ++k) {
+                    RowsEngine* r = ptrs[k];
+                    CHECK(r->row_lo() == bounds[k] * 32);
+                    const auto lv = r->finish();
+                    std::copy(lv.begin(), lv.end(), L.begin() + r->row_lo());
+                }
+                CHECK(L == rg.bfs(s, n));
+            }
+            // stepped: one host thread per rank, all-gather = device copies between barriers
+            auto st = make();
+            const std::uint64_t per = st[0]->per_words();
+            std::vector<std::uint32_t*> recv(world, nullptr);
+            for (auto& p : recv) CHECK(cudaMalloc(&p, world * per * 4) == cudaSuccess);
+            std::barrier sync(world);
+            auto gather = [&](const std::uint32_t*, std::uint32_t* out, std::uint64_t w) {
+                sync.arrive_and_wait();  // every rank's step of this level is enqueued
+                cudaDeviceSynchronize();
+                for (std::uint32_t k = 0; k < world; ++k)
+                    cudaMemcpy(out + k * w, st[k]->send_buffer(), w * 4, cudaMemcpyDeviceToDevice);
+                cudaDeviceSynchronize();
+                sync.arrive_and_wait();  // no rank overwrites its send buffer before all copied
+            };
+            for (VertexId s : srcs) {
+                std::vector<RowsOutcome> out(world);
+                std::vector<std::thread> th;
+                for (std::uint32_t k = 0; k < world; ++k)
+                    th.emplace_back([&, k] { out[k] = rows_bfs_stepped(*st[k], s, recv[k], gather); });
+                for (auto& t : th) t.join();
+                std::vector<Level> L(n, 0);
+                for (std::uint32_t k = 0; k < world; ++k) {
+                    CHECK(out[k].collectives == out[0].collectives && out[k].stats.iterations == out[0].stats.iterations);
+                    CHECK(out[k].collectives == out[k].stats.iterations + 1 + 2);
+                    std::copy(out[k].levels.begin(), out[k].levels.end(), L.begin() + st[k]->row_lo());
+                }
+                CHECK(L == rg.bfs(s, n));
+            }
+            for (auto p : recv) cudaFree(p);
         }
     }
     // BVSS cache + permutation files are the reference's: a file written by the reference's

@@ -11,6 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_facade_header_compiles():
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        "-I", os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include"),
                         os.path.join(ROOT, "tests", "cpp", "facade_test.cpp")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
 
