@@ -83,6 +83,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// Timing study (BLEST_XFLAGS bit `bit`): CTA 0's thread 0 stamps tstamp slot 1 of the level
+// once `dep` (a loaded value) has arrived — the volatile shared store consumes it first.
+__device__ __forceinline__ void probe(const Params& p, uint32_t level, uint32_t bit, uint32_t dep, bool first) {
+    if ((p.xflags & bit) && first && threadIdx.x == 0 && blockIdx.x == 0 && level - 1 < p.trace_cap) {
+        __shared__ uint32_t sink;
+        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sink)), "r"(dep)
+                     : "memory");
+        p.tstamp[3ull * (level - 1) + 1] = globaltimer();
+    }
+}
+
 // Fire-and-forget OR (REDG): the lazy scheme's "relaxed atomic" (R:src/bfs_engine.cpp:287-288).
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v));
@@ -315,7 +326,9 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
     // red_flag: set (plain store, every writer stores 1) when the CTA issued a stage-1 RED;
     // read back as the payload after the barrier
     if (red_flag && threadIdx.x == 0 && mine[2]) *red_flag = 1ull;
+    probe(p, level, 1u << 17, (uint32_t)mine[0], true);
     const uint32_t pay = grid_barrier_pay(p.bar, gen, red_flag ? red_flag : payload);
+    probe(p, level, 1u << 18, pay, true);
     if (threadIdx.x == 0) {
         const uint32_t row = min(level - 1, p.trace_cap - 1);
         unsigned long long* t = p.trace + 8ull * row;

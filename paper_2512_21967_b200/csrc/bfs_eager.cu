@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                 // atomicOr on F_next elects the discoverer (old bit clear) and its old byte
                 // says whether it is the set's first discovery this level (push, :204-205);
                 // (D) the discoverer stores the level and REDs its VIS bit.
+                const bool first = p0 == gw;
+                probe(p, level, 4096, mk[0] ^ rw[0].x ^ alpha_l, first);
                 uint32_t vw[4 * kBatch];
                 if (PULL == 0) {
 #pragma unroll
@@ -183,12 +185,14 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
 #pragma unroll
                     for (int k = 0; k < 4 * kBatch; ++k) vw[k] = recheck_word(Fn, row_of(rw, k), vw[k]);
                 }
+                probe(p, level, 8192, vw[0] ^ vw[1] ^ vw[2] ^ vw[3], first);
 #pragma unroll
                 for (int k = 0; k < 4 * kBatch; ++k) {
                     const uint32_t x = row_of(rw, k);
                     ctr[1] += ((vw[k] >> (x & 31)) & 1u) ^ 1u;  // full atomics (R:src/bfs_engine.cpp:203)
                     vw[k] = atom_if_clear(Fn, x, vw[k]);
                 }
+                probe(p, level, 16384, vw[0] ^ vw[1] ^ vw[2] ^ vw[3], first);
                 uint32_t disc = 0;
 #pragma unroll
                 for (int k = 0; k < 4 * kBatch; ++k) {
@@ -215,21 +219,27 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
                         const uint32_t x = row_of(rw, k);
                         const bool push = ((disc >> k) & 1u) && ((vw[k] >> (8 * ((x >> 3) & 3))) & 0xFFu) == 0;
                         push_column(p, push, (unsigned long long)(x >> 3) << 32 | (x >> 3), pbuf, pcount, Qn,
-                                    qlen_next, ctr[3], ctr[1], !recheck);
+                                    qlen_next, ctr[3], ctr[1], !recheck && !(p.xflags & 1024));
                     }
                 }
             }
         }
         if (pcount) {
-            const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next, !recheck);
+            const uint32_t t = flush_pushes(p, pbuf, pcount, Qn, qlen_next, !recheck && !(p.xflags & 1024));
             if (lane == 0) {
                 ctr[3] += t;
                 ctr[1] += 1;
             }
         }
+        probe(p, level, 32768, pcount, true);
         if (zss != 0xFFFFFFFFu) Fz[zss] = 0;
         for (uint64_t i = gtid + gthreads; i < prev_len; i += gthreads) Fz[Qz[i] >> 32] = 0;
         prev_len = len;
+        probe(p, level, 65536, ctr[0], true);
+        if ((p.xflags & (1u << 19)) && blockIdx.x == 0 && lane == 0 && level - 1 < p.trace_cap)  // timing study:
+            atomicMax(&p.tstamp[3ull * (level - 1) + 1], globaltimer());                      // CTA 0's last warp
+        if ((p.xflags & (1u << 20)) && lane == 0 && level - 1 < p.trace_cap)  // timing study: the grid's last warp
+            atomicMax(&p.tstamp[3ull * (level - 1) + 1], globaltimer());
         if ((p.xflags & 64) && threadIdx.x == 0 && level - 1 < p.trace_cap)  // timing study:
             atomicMax(&p.tstamp[3ull * (level - 1) + 1], globaltimer());      // last CTA's pull end
         next_len = level_barrier(p, sm, gen, level, ctr, 2, qlen_next);

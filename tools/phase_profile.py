@@ -58,8 +58,21 @@ def main():
                                stage1_us=round(s1, 2) if s1 is not None else None,
                                level_us=round(tot, 2), vss_GBps=round(648 * q / (tot * 1e3), 1) if tot else None))
         total_us = (ts[3 * (rows.value - 1) + 2] - ts[0]) / 1e3 if rows.value else 0
+        # every level, bucketed by queue size (high-diameter graphs: where the time goes)
+        hist = {}
+        for i in range(min(rows.value, cap)):
+            q = tr[i].queue_size
+            k = 0 if q == 0 else q.bit_length()
+            h = hist.setdefault(k, [0, 0.0, 0.0, 0])
+            h[0] += 1
+            h[1] += (ts[3 * i + 2] - ts[3 * i]) / 1e3
+            h[2] += ((ts[3 * i + 1] - ts[3 * i]) / 1e3) if ts[3 * i + 1] else 0.0
+            h[3] += q
+        buckets = [dict(queue_lt=1 << k, levels=h[0], total_us=round(h[1], 1), mean_level_us=round(h[1] / h[0], 2),
+                        mean_stage1_us=round(h[2] / h[0], 2), mean_queue=round(h[3] / h[0], 1))
+                   for k, h in sorted(hist.items())]
         out.append(dict(source=int(s), engine=mode.value, levels=levels, total_us=round(total_us, 2),
-                        dequeues=ctr.vss_dequeues))
+                        dequeues=ctr.vss_dequeues, iterations=rows.value, queue_buckets=buckets))
     print(json.dumps(dict(config=args.config, n=b.n, num_vss=b.num_vss, runs=out), indent=1))
 
 

@@ -1,0 +1,12 @@
+#!/bin/bash
+# cluster engine chain study on C4: tstamp slot 1 = CTA 0 warp 0 after each phase
+mkdir -p gpurun_out
+for x in 128 256 512 1024 2048; do
+BLEST_CLUSTER=1 BLEST_XFLAGS=$x timeout 600 python tools/phase_profile.py --config c4 --sources 1 > gpurun_out/cl_b_$x.json 2> gpurun_out/cl_b_$x.err
+python - $x <<'PY'
+import json, sys
+d = json.load(open(f"gpurun_out/cl_b_{sys.argv[1]}.json"))
+for r in d["runs"]:
+    print(sys.argv[1], r["iterations"], r["total_us"], [(b["queue_lt"], b["mean_stage1_us"], b["mean_level_us"]) for b in r["queue_buckets"]])
+PY
+done
