@@ -44,9 +44,6 @@ void* eager_kernel(int pull, int threads);       // bfs_eager.cu
 void* lazy_kernel(int pull, int threads, bool sigma);  // bfs_lazy.cu
 void* lazy_tma_kernel(int pull, int consumers);  // bfs_lazy_tma.cu (TMA producer/consumer)
 size_t lazy_tma_smem(int consumers);
-void* cluster_kernel(int threads);                // bfs_cluster.cu
-size_t cluster_smem(int threads);
-void cluster_init_launch(const bfsdev::Params& p, int ctas, cudaStream_t st);
 
 namespace {
 using namespace bfsdev;
@@ -138,14 +135,6 @@ uint64_t BfsEngine::prepare(const EngineOptions& opt) {
     return bytes;
 }
 
-// Eager levels on one thread-block cluster (bfs_cluster.cu): BLEST_CLUSTER=1 forces it,
-// =0 turns it off; by default (opt.cluster < 0) the eager popc engine uses it.
-bool BfsEngine::use_cluster_engine(const EngineOptions& opt) const {
-    if (opt.mode != Mode::Eager || opt.pull != Pull::Popc) return false;
-    if (const char* e = getenv("BLEST_CLUSTER")) return atoi(e) > 0;
-    return opt.cluster > 0;
-}
-
 void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (src >= b_.n) throw InvalidArgument("bfs source out of range");
     if (b_.num_sets >= (1u << 25)) throw InvalidArgument("the BFS engines support n < 2^28");
@@ -226,45 +215,10 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     if (const char* t = getenv("BLEST_TAIL_DIV")) p.tail_div = (uint32_t)atoi(t);
     if (const char* rc = getenv("BLEST_LAZY_RECHECK")) p.lazy_recheck = (uint32_t)atoi(rc);
     cudaStream_t st = stream();
-    if (use_cluster_engine(opt)) {  // bfs_cluster.cu: one thread-block cluster runs every level
-        const char* te = getenv("BLEST_CLUSTER_THREADS");
-        const int cthreads = te ? atoi(te) : 512;
-        void* ck = cluster_kernel(cthreads);
-        const size_t smem = cluster_smem(cthreads);
-        CK(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute(ck, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        const char* ce = getenv("BLEST_CLUSTER_SIZE");
-        unsigned csize = ce ? (unsigned)atoi(ce) : 16u;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        cudaLaunchConfig_t cfg{};
-        cfg.blockDim = dim3(cthreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        for (;; csize /= 2) {  // the largest cluster the device can place (16 needs a full GPC)
-            at[0].val.clusterDim.x = csize;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3(csize);
-            int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, ck, &cfg) == cudaSuccess && nc >= 1) break;
-            cudaGetLastError();
-            if (csize <= 1) throw CudaError("cluster engine cannot be resident");
-        }
-        cluster_init_launch(p, 4 * num_sms(), st);
-        CK(cudaGetLastError());
-        void* cargs[] = {&p};
-        CK(cudaLaunchKernelExC(&cfg, ck, cargs));
-        g_launches.fetch_add(2);
-        ctas = csize;
-    } else {
-        CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
-        void* args[] = {&p};
-        CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, dyn, st));
-        g_launches.fetch_add(1);
-    }
+    CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
+    void* args[] = {&p};
+    CK(cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(threads), args, dyn, st));
+    g_launches.fetch_add(1);
     last_levels_ = p.L;
     last_ctas_ = ctas;
     last_threads_ = threads;

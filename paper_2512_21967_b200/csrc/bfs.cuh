@@ -26,7 +26,6 @@ struct EngineOptions {
     uint32_t threads = 0;     // threads per CTA (256 / 512 / 1024); 0 = default
     bool sigma = true;        // lazy: hot-row view of the visited bitmaps (sigma.cuh)
     bool lazy_tma = false;    // lazy: TMA producer/consumer pipeline (measured slower on C2)
-    int cluster = 0;          // eager: run on one thread-block cluster (bfs_cluster.cu)
 };
 
 // One row per level, same fields as LevelTrace (R:include/blest/bfs_engine.hpp:27-37).
@@ -79,7 +78,6 @@ public:
 
 private:
     void ensure_sigma();
-    bool use_cluster_engine(const EngineOptions& opt) const;
     const DeviceBvss& b_;
     uint64_t words_ = 0, wstride_ = 0;
     uint32_t trace_cap_ = 0;
