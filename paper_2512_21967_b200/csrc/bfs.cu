@@ -214,6 +214,10 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.tail_div = 8;  // dense lazy levels hand out their last eighth dynamically
     if (const char* t = getenv("BLEST_TAIL_DIV")) p.tail_div = (uint32_t)atoi(t);
     if (const char* rc = getenv("BLEST_LAZY_RECHECK")) p.lazy_recheck = (uint32_t)atoi(rc);
+    // sparse lazy levels log their REDs' words (in Q0, unused then) so stage 2 visits those
+    // words only; beyond words/8 log entries the Θ(n/32) sweep is cheaper
+    p.log_cap = (uint32_t)std::min<uint64_t>(2 * qcap, std::max<uint64_t>(words_ / 8, 4096));
+    if (const char* sm = getenv("BLEST_SMALL_S2")) p.log_cap = atoi(sm) ? (uint32_t)atoll(sm) : 0u;
     cudaStream_t st = stream();
     CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
     void* args[] = {&p};

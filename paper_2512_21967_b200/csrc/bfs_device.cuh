@@ -53,6 +53,7 @@ struct Params {
     uint32_t xflags;  // experiment switches (BLEST_XFLAGS env; timing studies only)
     uint32_t lazy_recheck;  // lazy: test V_curr and re-check V_next at L2 (BLEST_LAZY_RECHECK)
     uint32_t tail_div;      // lazy: dense levels hand out their last 1/tail_div dynamically (0 = off)
+    uint32_t log_cap;       // lazy: dirty-word log entries (in Q0) for the small stage 2 (0 = off)
 };
 
 template <int THREADS, int MODE = 0>
@@ -577,6 +578,76 @@ __device__ __forceinline__ void lazy_stage2_hot(const Params& p, Smem<THREADS, 1
     if ((p.xflags & 32) && blockIdx.x == 0 && threadIdx.x == 0 && level - 1 < p.trace_cap)
         p.tstamp[3ull * (level - 1) + 1] = globaltimer();  // timing study: hot pass end
     lazy_stage2<THREADS, true>(p, sm, level, ctr, Fd);
+}
+
+// Small stage 2 (a sparse level whose stage-1 REDs all went into the dirty-word log,
+// lazy_pull.cuh RedLog): the same outputs as lazy_stage2(_hot) — V_curr = V_next, levels,
+// the next frontier words Fn (all zero beforehand) and the next level's SL — from the
+// logged words only, no Θ(n/32) sweep, no block scans, no extra grid barrier. Each logged
+// word is claimed with atomicOr(V_curr, V_next) (duplicates in the log find nothing new);
+// each discovery ORs its bit into Fn, and the lane that turns its set's byte nonzero owns
+// the set: it appends (first position << 32 | set) to SL with one warp-aggregated atomic on
+// the packed (sets, VSSs) counter `packed`, so SL stays ordered by first position (not by
+// set id) and exactly-once. Totals: packed's VSS part is the next T, its set part the next S.
+template <int THREADS, bool SIGMA>
+__device__ __forceinline__ void small_stage2(const Params& p, uint32_t level, uint32_t (&ctr)[4], uint32_t* Fn,
+                                             const uint32_t* log, uint32_t cnt, unsigned long long* packed) {
+    const unsigned lane = lane_id();
+    const uint32_t gw = blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
+    const uint32_t all_warps = gridDim.x * (THREADS / 32);
+    const uint64_t hw = SIGMA ? p.hot_words : 0;
+    uint32_t* Vc = p.B0;
+    const uint32_t* Vn = p.B1;
+    for (uint64_t base = (uint64_t)gw * 32; base < cnt; base += (uint64_t)all_warps * 32) {
+        const uint64_t i = base + lane;
+        uint32_t d = 0, we = 0;
+        if (i < cnt) {
+            we = log[i];
+            const uint32_t nx = __ldcg(Vn + we);
+            d = nx & ~atomicOr(Vc + we, nx);
+        }
+        // the warp's discoveries, 32 per round, whatever word they sit in (a hub word of the
+        // hot prefix holds up to 32): lane k takes the k-th set bit of the concatenation
+        const uint32_t nb = __popc(d);
+        ctr[0] += nb;
+        const uint32_t incl = warp_incl_scan(nb), excl = incl - nb;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            int l = 0;  // the last lane with excl <= k: the word holding discovery k
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1)
+                if (__shfl_sync(0xffffffffu, excl, l + step) <= k) l += step;
+            const uint32_t dw = __shfl_sync(0xffffffffu, d, l), wl = __shfl_sync(0xffffffffu, we, l);
+            const uint32_t jth = k - __shfl_sync(0xffffffffu, excl, l);
+            bool own = false;
+            uint32_t r = 0;
+            if (k < total) {
+                const uint32_t b = __fns(dw, 0, jth + 1);
+                r = (SIGMA && wl < hw) ? __ldg(p.inv + 32ull * wl + b) : 32u * (uint32_t)(wl - hw) + b;
+                p.L[r] = level;
+                const uint32_t o = atomicOr(Fn + (r >> 5), 1u << (r & 31));
+                own = ((o >> (8 * ((r >> 3) & 3))) & 0xFFu) == 0;
+            }
+            const uint32_t ss = r >> 3;
+            uint32_t c = 0;
+            if (own) c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
+            const unsigned long long v = c ? pack_vs(c, 1) : 0ull;
+            unsigned long long vin = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, vin, o);
+                if (lane >= (unsigned)o) vin += y;
+            }
+            unsigned long long at = 0;
+            if (lane == 31 && vin) at = atomicAdd(packed, vin);
+            at = __shfl_sync(0xffffffffu, at, 31) + vin - v;
+            if (c) {
+                p.SL[at >> (64 - kSetBits)] = ((at & kVssMask) << 32) | ss;
+                ctr[3] += c;
+            }
+        }
+    }
 }
 
 }  // namespace bfsdev

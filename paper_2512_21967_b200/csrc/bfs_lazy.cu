@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         p.SL[0] = sset;                        // first position 0
         p.ctl[0] = seed_e - seed_b;            // T: VSSs queued for the level
         p.ctl[1] = (seed_e > seed_b) ? 1 : 0;  // S: slice sets queued
-        for (int i = 2; i < 8; ++i) p.ctl[i] = 0;
+        for (int i = 2; i < 16; ++i) p.ctl[i] = 0;
         for (int i = 0; i < 8; ++i) p.trace[i] = 0;
     }
     uint32_t next_T = grid_barrier_pay(p.bar, gen, &p.ctl[0]);
@@ -91,10 +91,14 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
     for (uint64_t i = gtid; i < p.n; i += gthreads) p.L[i] = (i == src) ? 0u : kInf;
 
     uint32_t ctr[4] = {0, 0, 0, 0};  // discovered, full, relaxed, pushes
+    bool prev_small = false;  // the last stage 2 was small_stage2 (uniform over the grid)
     uint32_t level = 1;
     for (;; ++level) {
         const unsigned long long len = next_T;  // broadcast by the barrier
-        const uint32_t S = (uint32_t)ld_relaxed_gpu_u64(&p.ctl[1]);
+        // S: the full stage 2 stores it in ctl[1]; small_stage2 packs it with T (ctl[8|9])
+        const uint32_t S = prev_small
+                               ? (uint32_t)(ld_relaxed_gpu_u64(&p.ctl[8 + ((level - 1) & 1)]) >> (64 - kSetBits))
+                               : (uint32_t)ld_relaxed_gpu_u64(&p.ctl[1]);
         if (len == 0) break;
         if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
             if (gtid == 0) p.ctl[6] = 1;
@@ -103,6 +107,8 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         if (gtid == 0) {
             p.ctl[7] = 0;  // stage-1 tail chunk counter (read after the expansion barrier)
             p.ctl[2 + ((level + 1) & 1)] = 0;  // the next level's RED flag (last read at level - 1)
+            p.ctl[8 + (level & 1)] = 0;         // small stage 2 counter (last read at level - 1's start)
+            p.ctl[10 + ((level + 1) & 1)] = 0;  // the next level's dirty-word log count
             if (level - 1 < p.trace_cap) {
                 p.trace[8ull * (level - 1) + 0] = level;
                 p.trace[8ull * (level - 1) + 1] = len;
@@ -139,10 +145,15 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         pc.NW = NW;
         pc.all_warps = all_warps;
         pc.pol = pol;
-        if (len < p.dense_min) {
-            if (SIGMA)  // Fn is the previous level's α: its readers finished long ago
-                for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
-            ctr[2] += pull_sparse<PULL>(pc);
+        const bool sparse = len < p.dense_min;
+        if (sparse) {
+            // Fn is the previous level's α (its readers finished long ago): cleared here for
+            // the hot view's stage 2 and for small_stage2, which writes only discoveries
+            for (uint64_t w = gtid; w < p.words; w += gthreads) Fn[w] = 0;
+            pc.log.words = reinterpret_cast<uint32_t*>(p.Q0);  // the queue is unused on sparse levels
+            pc.log.count = &p.ctl[10 + (level & 1)];
+            pc.log.cap = p.log_cap;
+            ctr[2] += pull_sparse<PULL, true>(pc);
         } else {
             expand_queue(pc);
             if (SIGMA)
@@ -154,17 +165,27 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         // No RED this level ⇔ no discovery (a RED is the only way a V_next bit gets set, and
         // the barrier before the stage made every earlier bit visible to the tests): the
         // level is the barren last one — skip its Θ(n/32) stage 2 (one per BFS, ~17 µs).
-        if (level_barrier(p, sm, gen, level, ctr, 1, nullptr, &p.ctl[2 + (level & 1)]) == 0) {
+        // (sparse levels: the payload is the dirty-word log count, zero iff no RED)
+        const uint32_t s1 = sparse ? level_barrier(p, sm, gen, level, ctr, 1, &p.ctl[10 + (level & 1)])
+                                   : level_barrier(p, sm, gen, level, ctr, 1, nullptr, &p.ctl[2 + (level & 1)]);
+        if (s1 == 0) {
             if (gtid == 0 && level - 1 < p.trace_cap) p.tstamp[3ull * (level - 1) + 2] = globaltimer();
             ++level;  // the barren level counts as an iteration (R:src/bfs_engine.cpp:117-124)
             break;
         }
 
-        if (SIGMA)
-            lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen, Fn);
-        else
-            lazy_stage2<THREADS>(p, sm, level, ctr, Fn);
-        next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);
+        prev_small = sparse && s1 <= p.log_cap;  // the log holds every RED'd word
+        if (prev_small) {
+            small_stage2<THREADS, SIGMA>(p, level, ctr, Fn, reinterpret_cast<const uint32_t*>(p.Q0), s1,
+                                         &p.ctl[8 + (level & 1)]);
+            next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[8 + (level & 1)]);
+        } else {
+            if (SIGMA)
+                lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen, Fn);
+            else
+                lazy_stage2<THREADS>(p, sm, level, ctr, Fn);
+            next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);
+        }
     }
     if (gtid == 0) p.ctl[4] = level - 1;
 }

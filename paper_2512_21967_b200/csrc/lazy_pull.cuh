@@ -39,9 +39,19 @@ namespace bfsdev {
 // (Codegen note: the optional phase B branch also keeps ptxas from interleaving phase A's
 // result moves with its later loads — without it the same default path measured 5.3 ms
 // per BFS instead of 2.0.)
-template <typename Hit>
+// LOG (sparse levels of the single-GPU kernel): every word a RED went to is appended to the
+// level's dirty-word log (one reservation per warp and batch), so a small stage 2 can visit
+// just those words instead of sweeping all n/32 (bfs_device.cuh small_stage2).
+struct RedLog {
+    uint32_t* words;             // log entries (engine word index; duplicates allowed)
+    unsigned long long* count;   // entries reserved (may exceed cap: then the log is incomplete)
+    uint32_t cap;
+};
+
+template <bool LOG = false, typename Hit>
 __device__ __forceinline__ uint32_t check_batch(const uint32_t* W, uint32_t* Vn, bool recheck, uint32_t sent,
-                                                const uint4 (&rw)[kBatchLazy], Hit hit) {
+                                                const uint4 (&rw)[kBatchLazy], Hit hit, const RedLog* log = nullptr,
+                                                bool* log_on = nullptr) {
     uint32_t vw[4 * kBatchLazy];
 #pragma unroll
     for (int j = 0; j < kBatchLazy; ++j) {
@@ -57,7 +67,7 @@ __device__ __forceinline__ uint32_t check_batch(const uint32_t* W, uint32_t* Vn,
             for (int c = 0; c < 4; ++c) vw[4 * j + c] = recheck_word(Vn, u[c], vw[4 * j + c]);
         }
     }
-    uint32_t reds = 0;
+    uint32_t reds = 0, issued = 0;
 #pragma unroll
     for (int j = 0; j < kBatchLazy; ++j) {
         const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
@@ -69,7 +79,27 @@ __device__ __forceinline__ uint32_t check_batch(const uint32_t* W, uint32_t* Vn,
             if (!(vw[4 * j + c] & bit)) {
                 red_or(Vn + (u[c] >> 5), bit);
                 ++reds;
+                if (LOG) issued |= 1u << (4 * j + c);
             }
+        }
+    }
+    if (LOG && *log_on && __any_sync(0xffffffffu, issued != 0)) {
+        const uint32_t n = __popc(issued);
+        const uint32_t incl = warp_incl_scan(n);
+        unsigned long long base = 0;
+        if (lane_id() == 31) base = atomicAdd(log->count, (unsigned long long)incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        if (base + __shfl_sync(0xffffffffu, incl, 31) > log->cap) *log_on = false;  // full: stop logging
+        base += incl - n;
+#pragma unroll
+        for (int j = 0; j < kBatchLazy; ++j) {
+            const uint32_t u[4] = {rw[j].x, rw[j].y, rw[j].z, rw[j].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if ((issued >> (4 * j + c)) & 1u) {
+                    if (base < log->cap) log->words[base] = u[c] >> 5;
+                    ++base;
+                }
         }
     }
     return reds;
@@ -93,6 +123,7 @@ struct PullCtx {
     uint32_t tail_div;
     uint32_t gw, NW, all_warps;          // this warp, pulling warps, all warps of the grid
     uint64_t pol;                        // L2 evict-first policy for the BVSS stream
+    RedLog log;                          // pull_sparse<PULL, true>: dirty-word log
 };
 
 // Every pointer of the context addresses global memory. Callers whose pointers come from a
@@ -180,8 +211,8 @@ __device__ __forceinline__ unsigned long long entry_at(const PullCtx& c, uint64_
 // Loads of the VSSs named by lanes 0..kBatchLazy-1 of e, then their visited tests. An
 // absent batch slot carries entry 0 (VSS 0 with α = 0): its loads are harmless and its
 // pull finds no candidate, so no per-slot predication is needed.
-template <int PULL>
-__device__ __forceinline__ uint32_t pull_batch(const PullCtx& c, unsigned long long e) {
+template <int PULL, bool LOG = false>
+__device__ __forceinline__ uint32_t pull_batch(const PullCtx& c, unsigned long long e, bool* log_on = nullptr) {
     const unsigned lane = lane_id();
     uint32_t mk[kBatchLazy], a[kBatchLazy];
     uint4 rw[kBatchLazy];
@@ -196,8 +227,8 @@ __device__ __forceinline__ uint32_t pull_batch(const PullCtx& c, unsigned long l
         uint32_t x[kBatchLazy];  // mask & α in every column byte
 #pragma unroll
         for (int j = 0; j < kBatchLazy; ++j) x[j] = mk[j] & (a[j] * 0x01010101u);
-        return check_batch(c.W, c.Vn, c.recheck, c.sent, rw,
-                           [&](int j, int col) { return (x[j] & (0xFFu << (8 * col))) != 0u; });
+        return check_batch<LOG>(c.W, c.Vn, c.recheck, c.sent, rw,
+                                [&](int j, int col) { return (x[j] & (0xFFu << (8 * col))) != 0u; }, &c.log, log_on);
     }
     uint32_t cm[kBatchLazy];  // column hits from the b1 tile (bit c = column c)
 #pragma unroll
@@ -206,12 +237,13 @@ __device__ __forceinline__ uint32_t pull_batch(const PullCtx& c, unsigned long l
         column_counts<PULL>(mk[j], a[j], cnt);
         cm[j] = (cnt[0] != 0) | ((cnt[1] != 0) << 1) | ((cnt[2] != 0) << 2) | ((cnt[3] != 0) << 3);
     }
-    return check_batch(c.W, c.Vn, c.recheck, c.sent, rw, [&](int j, int col) { return ((cm[j] >> col) & 1u) != 0u; });
+    return check_batch<LOG>(c.W, c.Vn, c.recheck, c.sent, rw,
+                            [&](int j, int col) { return ((cm[j] >> col) & 1u) != 0u; }, &c.log, log_on);
 }
 
 // Sparse level: the warp expands its own contiguous share of the queue and pulls it
 // straight from registers — no materialised queue, no barrier. Returns REDs issued.
-template <int PULL>
+template <int PULL, bool LOG = false>
 __device__ __forceinline__ uint32_t pull_sparse(const PullCtx& c) {
     assume_global(c);
     uint32_t reds = 0;
@@ -221,13 +253,14 @@ __device__ __forceinline__ uint32_t pull_sparse(const PullCtx& c) {
     if (lo >= hi) return 0;
     SetWindow win;
     load_window(c.SL, c.rp, c.Fd8, find_set(c.SL, c.S, lo), c.S, c.len, win);
+    bool log_on = true;  // LOG: until the log is full (then stage 2 sweeps anyway)
     for (uint64_t c0 = lo; c0 < hi; c0 += 32) {
         const unsigned long long mine = entry_at(c, c0, win);
         const uint32_t cnt = (hi - c0 < 32) ? (uint32_t)(hi - c0) : 32u;
         for (uint32_t k = 0; k < cnt; k += kBatchLazy) {
             unsigned long long e = __shfl_sync(0xffffffffu, mine, (lane + k) & 31);
             if (lane >= (uint32_t)kBatchLazy || k + lane >= cnt) e = 0;  // absent
-            reds += pull_batch<PULL>(c, e);
+            reds += pull_batch<PULL, LOG>(c, e, &log_on);
         }
     }
     return reds;
