@@ -217,7 +217,8 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     // sparse lazy levels log their REDs' words (in Q0, unused then) so stage 2 visits those
     // words only; beyond words/8 log entries the Θ(n/32) sweep is cheaper
     p.log_cap = (uint32_t)std::min<uint64_t>(2 * qcap, std::max<uint64_t>(words_ / 8, 4096));
-    if (const char* sm = getenv("BLEST_SMALL_S2")) p.log_cap = atoi(sm) ? (uint32_t)atoll(sm) : 0u;
+    if (const char* sm = getenv("BLEST_SMALL_S2"))  // the log lives in Q0: at most 2·qcap entries
+        p.log_cap = (uint32_t)std::min<uint64_t>((uint64_t)std::max(0ll, atoll(sm)), 2 * qcap);
     cudaStream_t st = stream();
     CK(cudaMemsetAsync(bar_.p, 0, 4 * sizeof(unsigned), st));
     void* args[] = {&p};

@@ -254,6 +254,9 @@ def test_auto_pipeline_maps_levels_back(oracle):
     {"BLEST_DENSE_MIN": "1", "BLEST_TAIL_DIV": "2"},  # lazy: dense levels, last half handed out dynamically
     {"BLEST_DENSE_MIN": "1", "BLEST_TAIL_DIV": "0"},  # lazy: dense levels, static round-robin only
     {"BLEST_LAZY_VARIANT": "tma"},         # lazy: TMA producer/consumer stage 1 (ablation)
+    {"BLEST_SMALL_S2": "0"},               # lazy: every stage 2 sweeps all words (no dirty-word log)
+    {"BLEST_SMALL_S2": "48"},              # lazy: tiny log — small stage 2 only where it fits, sweep elsewhere
+    {"BLEST_DENSE_MIN": "1000000000", "BLEST_SMALL_S2": "100000000"},  # lazy: every level sparse, log as large as Q0
 ])
 def test_engine_phase_variants(oracle, monkeypatch, env):
     """The batch-wide visited-test phases, the lazy σ view and their switches change only how
