@@ -357,19 +357,42 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
 // predecessors'; pass B writes its SL entries (set | first position << 32) in ascending
 // order, reusing the diff words held in registers when the CTA owns one chunk. The last
 // CTA stores the grid totals (the next level's T, S) in ctl[0], ctl[1].
+// The 17 real_ptrs entries bounding the 16 slice sets of words w0 … w0+3 (sets 4·w0 …
+// 4·w0+15), issued together — four 16-byte loads (4·w0 is a multiple of 16) and one word —
+// instead of up to 16 dependent pairs behind per-byte branches. Past the last set the
+// bound repeats (count 0).
+__device__ __forceinline__ void s2_rp(const Params& p, uint64_t w0, uint32_t (&r)[17]) {
+    const uint64_t s0 = 4 * w0;
+    if (s0 + 16 <= p.num_sets) {
+        const uint4* q = reinterpret_cast<const uint4*>(p.rp + s0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 v = __ldg(q + i);
+            r[4 * i] = v.x;
+            r[4 * i + 1] = v.y;
+            r[4 * i + 2] = v.z;
+            r[4 * i + 3] = v.w;
+        }
+        r[16] = __ldg(p.rp + s0 + 16);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 17; ++i) r[i] = __ldg(p.rp + min(s0 + i, (uint64_t)p.num_sets));
+    }
+}
+
 template <int THREADS>
 __device__ __forceinline__ void s2_counts(const Params& p, uint64_t w0, const uint32_t (&d)[4],
                                           unsigned long long& nv, unsigned long long& ns) {
+    if (!(d[0] | d[1] | d[2] | d[3])) return;
+    uint32_t r[17];
+    s2_rp(p, w0, r);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            if ((d[k] >> (8 * b)) & 0xFFu) {
-                const uint64_t ss = 4 * (w0 + k) + b;
-                const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
-                nv += c;
-                ns += c != 0;  // sets without VSSs push nothing
-            }
+            const uint32_t c = ((d[k] >> (8 * b)) & 0xFFu) ? r[4 * k + b + 1] - r[4 * k + b] : 0u;
+            nv += c;
+            ns += c != 0;  // sets without VSSs push nothing
         }
     }
 }
@@ -453,17 +476,16 @@ __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm
         unsigned long long pv = run_vss + (pos & kVssMask);
         unsigned long long ps = run_sets + (pos >> (64 - kSetBits));
         if (ns) {
+            uint32_t r[17];
+            s2_rp(p, w0, r);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    if ((d[k] >> (8 * b)) & 0xFFu) {
-                        const uint64_t ss = 4 * (w0 + k) + b;
-                        const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
-                        if (c) {
-                            p.SL[ps++] = (pv << 32) | ss;
-                            pv += c;
-                        }
+                    const uint32_t c = ((d[k] >> (8 * b)) & 0xFFu) ? r[4 * k + b + 1] - r[4 * k + b] : 0u;
+                    if (c) {
+                        p.SL[ps++] = (pv << 32) | (4 * (w0 + k) + b);
+                        pv += c;
                     }
                 }
             }
