@@ -361,10 +361,10 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
 // 4·w0+15), issued together — four 16-byte loads (4·w0 is a multiple of 16) and one word —
 // instead of up to 16 dependent pairs behind per-byte branches. Past the last set the
 // bound repeats (count 0).
-__device__ __forceinline__ void s2_rp(const Params& p, uint64_t w0, uint32_t (&r)[17]) {
+__device__ __forceinline__ void s2_rp(const uint32_t* rp, uint64_t num_sets, uint64_t w0, uint32_t (&r)[17]) {
     const uint64_t s0 = 4 * w0;
-    if (s0 + 16 <= p.num_sets) {
-        const uint4* q = reinterpret_cast<const uint4*>(p.rp + s0);
+    if (s0 + 16 <= num_sets) {
+        const uint4* q = reinterpret_cast<const uint4*>(rp + s0);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint4 v = __ldg(q + i);
@@ -373,10 +373,10 @@ __device__ __forceinline__ void s2_rp(const Params& p, uint64_t w0, uint32_t (&r
             r[4 * i + 2] = v.z;
             r[4 * i + 3] = v.w;
         }
-        r[16] = __ldg(p.rp + s0 + 16);
+        r[16] = __ldg(rp + s0 + 16);
     } else {
 #pragma unroll
-        for (int i = 0; i < 17; ++i) r[i] = __ldg(p.rp + min(s0 + i, (uint64_t)p.num_sets));
+        for (int i = 0; i < 17; ++i) r[i] = __ldg(rp + min(s0 + i, num_sets));
     }
 }
 
@@ -385,7 +385,7 @@ __device__ __forceinline__ void s2_counts(const Params& p, uint64_t w0, const ui
                                           unsigned long long& nv, unsigned long long& ns) {
     if (!(d[0] | d[1] | d[2] | d[3])) return;
     uint32_t r[17];
-    s2_rp(p, w0, r);
+    s2_rp(p.rp, p.num_sets, w0, r);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
 #pragma unroll
@@ -477,7 +477,7 @@ __device__ __forceinline__ void s2_enqueue(const Params& p, Smem<THREADS, 1>& sm
         unsigned long long ps = run_sets + (pos >> (64 - kSetBits));
         if (ns) {
             uint32_t r[17];
-            s2_rp(p, w0, r);
+            s2_rp(p.rp, p.num_sets, w0, r);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
 #pragma unroll

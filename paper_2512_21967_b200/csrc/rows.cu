@@ -172,17 +172,19 @@ __device__ unsigned long long stage2b(const RowsParams& p, Smem<THREADS, 1>& sm,
             d[k] = v;
         }
     };
+    const uint64_t num_sets = (p.n + 7ull) / 8;
     auto counts = [&](uint64_t w0, const uint32_t (&d)[4], unsigned long long& nv, unsigned long long& ns) {
+        if (!(d[0] | d[1] | d[2] | d[3])) return;
+        uint32_t r[17];  // the 16 sets' real_ptrs bounds, loaded together (bfs_device.cuh s2_rp)
+        s2_rp(p.rp, num_sets, w0, r);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((d[k] >> (8 * b)) & 0xFFu) {
-                    const uint64_t ss = 4 * (w0 + k) + b;
-                    const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
-                    nv += c;
-                    ns += c != 0;
-                }
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t c = ((d[k] >> (8 * b)) & 0xFFu) ? r[4 * k + b + 1] - r[4 * k + b] : 0u;
+                nv += c;
+                ns += c != 0;
+            }
     };
     unsigned long long my_v = 0, my_s = 0, my_b = 0, nzm = 0;
     if (threadIdx.x == 0) sm.nz = 0;
@@ -282,18 +284,18 @@ __device__ unsigned long long stage2b(const RowsParams& p, Smem<THREADS, 1>& sm,
         unsigned long long pv = run_v + block_excl_scan(sm, nv, &it_v);
         unsigned long long ps = run_s + block_excl_scan(sm, ns, &it_s);
         if (ns) {
+            uint32_t r[17];
+            s2_rp(p.rp, num_sets, w0, r);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
 #pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if ((d[k] >> (8 * b)) & 0xFFu) {
-                        const uint64_t ss = 4 * (w0 + k) + b;
-                        const uint32_t c = __ldg(p.rp + ss + 1) - __ldg(p.rp + ss);
-                        if (c) {
-                            p.SL[ps++] = (pv << 32) | ss;
-                            pv += c;
-                        }
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t c = ((d[k] >> (8 * b)) & 0xFFu) ? r[4 * k + b + 1] - r[4 * k + b] : 0u;
+                    if (c) {
+                        p.SL[ps++] = (pv << 32) | (4 * (w0 + k) + b);
+                        pv += c;
                     }
+                }
         }
         run_v += it_v;
         run_s += it_s;
