@@ -220,6 +220,33 @@ def engine_policy_lazy(n: int, m: int, num_vss: int) -> bool:
     return m >= 8 * max(n, 1) and num_vss >= (1 << 20)
 
 
+def batch_d2h_bytes(deepest: list, n: int, packed: bool) -> int:
+    """Level bytes one blest_bfs_batch call moves over PCIe (BfsEngine::run_batch, xfer.cuh):
+    source k goes at the width in force when it launched (1 byte, then 2, then u32); a source
+    whose deepest level does not fit is re-copied as u32 once its copy lands (two sources
+    later), which also widens the sources launched after that."""
+    if not packed:
+        return 4 * n * len(deepest)
+    width, wk, total = 1, [0] * len(deepest), 0
+
+    def fin(j):
+        nonlocal width
+        if not wk[j] or deepest[j] < (255 if wk[j] == 1 else 65535):
+            return 0
+        if width == wk[j]:
+            width = 2 if (wk[j] == 1 and deepest[j] < 65535) else 0
+        return 4 * n
+
+    for k in range(len(deepest)):
+        if k >= 2:
+            total += fin(k - 2)
+        wk[k] = width
+        total += wk[k] * n + 8 if wk[k] else 4 * n
+    for j in range(max(0, len(deepest) - 2), len(deepest)):
+        total += fin(j)
+    return total
+
+
 def prepare(config: str, ordering_override: str | None, window: int, build: bool = True):
     """Generate -> (relabel) -> plan/order -> permute -> build, all on the GPU (build=False:
     the row-partitioned mode builds one BVSS slice per rank instead)."""
@@ -600,6 +627,8 @@ def main():
         cbuf = (L.CountersT * chunk)()
         torch.cuda.synchronize()
         te = np.zeros(len(mine))
+        d2h = 0  # level bytes over PCIe, per blest_bfs_batch's width rule (xfer.cuh)
+        packed = os.environ.get("BLEST_D2H_PACK", "1") != "0"
         for c0 in range(0, len(mine), chunk):
             part = np.ascontiguousarray(mine[c0:c0 + chunk], np.uint32)
             t0 = time.perf_counter()
@@ -607,11 +636,14 @@ def main():
             L.check(lib.blest_bfs_batch(b.handle, C.c_void_p(hsrc.data_ptr()), len(part), C.byref(ecfg),
                                         C.c_void_p(hl.data_ptr()), C.cast(cbuf, C.c_void_p)))
             te[c0:c0 + len(part)] = (time.perf_counter() - t0) / len(part)
+            d2h += batch_d2h_bytes([c.levels_processed for c in list(cbuf)[: len(part)]], n, packed)
         e2e_hm = len(te) / float(np.sum(te / E)) / 1e9
         e2e = dict(value=round(e2e_hm * world, 4), unit="GTEPS", h2d_bytes_per_step=4,
-                   d2h_bytes_per_step=int(4 * n + 8 * 8 + 16),
+                   d2h_bytes_per_step=int(d2h / len(mine)) + 8 * 8 + 16,
                    note=f"blest_bfs_batch() in chunks of {chunk} sources: source ids in, every source's full "
-                        "level array (pinned host) + counters out, host wall clock per chunk / chunk size")
+                        "u32 level array (pinned host) + counters out, host wall clock per chunk / chunk size; "
+                        + ("levels cross PCIe as (level+1) in 1-2 bytes and host threads widen them to u32 "
+                           "inside the call" if packed else "levels cross PCIe as u32 (BLEST_D2H_PACK=0)"))
 
     # ---- CPU baseline (rank 0, N = 1 only): every host core again ----
     os.sched_setaffinity(0, all_cpus)

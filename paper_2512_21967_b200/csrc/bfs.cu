@@ -28,8 +28,11 @@
 // pass B writes its slice sets' VSS ranges at that offset. The next queue is therefore in
 // ascending slice-set order — deterministic, and stage 1 then streams the BVSS in address
 // order — with no contended queue-tail atomic at all.
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "bfs.cuh"
@@ -101,7 +104,31 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
 }
 
 BfsEngine::~BfsEngine() {
+    pool_.reset();
     if (pinned_) cudaFreeHost(pinned_);
+    if (stage_) cudaFreeHost(stage_);
+    if (stage_max_) cudaFreeHost(stage_max_);
+}
+
+// Widening threads: the CPUs this process may run on (bench.py pins it to the GPU's NUMA
+// node) minus the launching thread; BLEST_XFER_THREADS overrides.
+static int xfer_threads() {
+    if (const char* t = getenv("BLEST_XFER_THREADS")) return std::max(1, atoi(t));
+    cpu_set_t set;
+    int cpus = 8;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) cpus = CPU_COUNT(&set);
+    return std::min(32, std::max(1, cpus - 1));
+}
+
+void BfsEngine::ensure_xfer() {
+    if (!levels2_.p) levels2_.alloc(b_.n ? b_.n : 1);
+    if (stage_ || !b_.n) return;
+    const uint64_t slot = 2ull * b_.n;
+    dpack_.alloc(2 * slot);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_), kStageRing * slot, cudaHostAllocDefault));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_max_), kStageRing * sizeof(unsigned long long),
+                     cudaHostAllocDefault));
+    pool_.reset(new WidenPool(xfer_threads()));
 }
 
 void BfsEngine::ensure_sigma() {
@@ -126,8 +153,9 @@ void BfsEngine::ensure_sigma() {
 uint64_t BfsEngine::prepare(const EngineOptions& opt) {
     const char* sig_env = getenv("BLEST_SIGMA");
     if (opt.mode == Mode::Lazy && opt.sigma && !(sig_env && atoi(sig_env) == 0)) ensure_sigma();
+    ensure_xfer();
     CK(cudaStreamSynchronize(stream()));
-    uint64_t bytes = levels_.count * 4 + levels2_.count * 4 + bits_.count * 4 + q_.count * 8 + ctl_.count * 8 +
+    uint64_t bytes = levels_.count * 4 + levels2_.count * 4 + dpack_.count + bits_.count * 4 + q_.count * 8 + ctl_.count * 8 +
                      agg_.count * 8 + aggS_.count * 8 + sl_.count * 8 + bar_.count * 4 + trace_.count * 8 +
                      tstamp_.count * 8;
     if (sigma_on_)
@@ -238,7 +266,13 @@ std::vector<BfsOutcome> BfsEngine::run_batch(const uint32_t* srcs, uint32_t coun
         if (srcs[k] >= b_.n) throw InvalidArgument("bfs source out of range");
     std::vector<BfsOutcome> outs(count);
     if (!count) return outs;
-    if (!levels2_.p) levels2_.alloc(b_.n ? b_.n : 1);
+    const uint64_t n = b_.n;
+    // narrow transfers (xfer.cuh) unless BLEST_D2H_PACK=0: width 1, then 2, then plain u32
+    // once a source's deepest level does not fit
+    const char* pk = getenv("BLEST_D2H_PACK");
+    const bool pack = levels_host && n && !(pk && atoi(pk) == 0);
+    if (pack) ensure_xfer();
+    if (!levels2_.p) levels2_.alloc(n ? n : 1);
     DevBuf<unsigned long long> summ(8ull * count);
     cudaStream_t st = stream(), cp = nullptr;
     cudaEvent_t kern_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
@@ -248,28 +282,82 @@ std::vector<BfsOutcome> BfsEngine::run_batch(const uint32_t* srcs, uint32_t coun
         CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
     }
     uint32_t* bufs[2] = {levels_.p, levels2_.p};
+    const uint64_t slot = 2 * n;
+    int width = 1;
+    std::vector<int> wk(count, 0);  // transfer width of source k (0 = u32 copy)
+    std::vector<WidenPool::Job> jobs(count);
+    std::vector<char> live(count, 0);
+    auto drain = [&] {
+        for (uint32_t j = 0; j < count; ++j)
+            if (live[j]) {
+                pool_->wait(&jobs[j]);
+                live[j] = 0;
+            }
+    };
+    // host side of source j once its copy has landed: widen it, or fetch the exact u32
+    // array (still in its device buffer: the BFS two sources later waits for copy_done)
+    auto finalize = [&](uint32_t j) {
+        if (!wk[j]) return;
+        const int s = j & 1;
+        CK(cudaEventSynchronize(copy_done[s]));
+        const unsigned long long deepest = stage_max_[j % kStageRing];
+        const int w = wk[j];
+        if (deepest < (w == 1 ? 255ull : 65535ull)) {
+            WidenPool::Job& jb = jobs[j];
+            jb.in = stage_ + (j % kStageRing) * slot;
+            jb.width = w;
+            jb.out = levels_host + (uint64_t)j * n;
+            jb.n = n;
+            pool_->submit(&jb);
+            live[j] = 1;
+        } else {
+            CK(cudaMemcpyAsync(levels_host + (uint64_t)j * n, bufs[s], (size_t)n * 4, cudaMemcpyDeviceToHost, cp));
+            CK(cudaEventRecord(copy_done[s], cp));
+            if (width == w) width = (w == 1 && deepest < 65535ull) ? 2 : 0;
+        }
+    };
     try {
         for (uint32_t k = 0; k < count; ++k) {
             const int s = k & 1;
-            if (k >= 2) CK(cudaStreamWaitEvent(st, copy_done[s], 0));  // buffer s free again
+            if (k >= 2) {
+                finalize(k - 2);
+                CK(cudaStreamWaitEvent(st, copy_done[s], 0));  // buffer s free again
+            }
             level_target_ = bufs[s];
             launch(srcs[k], opt);
             level_target_ = nullptr;
             k_summarise<<<1, 256, 0, st>>>(ctl_.p, trace_.p, trace_cap_, summ.p + 8ull * k);
             CK(cudaGetLastError());
+            wk[k] = pack ? width : 0;
+            if (wk[k]) pack_levels(bufs[s], n, wk[k], dpack_.p + s * slot, st);
             CK(cudaEventRecord(kern_done[s], st));
-            if (levels_host && b_.n) {
+            if (levels_host && n) {
                 CK(cudaStreamWaitEvent(cp, kern_done[s], 0));
-                CK(cudaMemcpyAsync(levels_host + (uint64_t)k * b_.n, bufs[s], (size_t)b_.n * 4,
-                                   cudaMemcpyDeviceToHost, cp));
+                if (wk[k]) {
+                    const uint32_t r = k % kStageRing;
+                    if (k >= (uint32_t)kStageRing && live[k - kStageRing]) {  // staging slot r free
+                        pool_->wait(&jobs[k - kStageRing]);
+                        live[k - kStageRing] = 0;
+                    }
+                    CK(cudaMemcpyAsync(stage_ + r * slot, dpack_.p + s * slot, (size_t)n * wk[k],
+                                       cudaMemcpyDeviceToHost, cp));
+                    CK(cudaMemcpyAsync(stage_max_ + r, summ.p + 8ull * k + 1, 8, cudaMemcpyDeviceToHost, cp));
+                } else {
+                    CK(cudaMemcpyAsync(levels_host + (uint64_t)k * n, bufs[s], (size_t)n * 4,
+                                       cudaMemcpyDeviceToHost, cp));
+                }
             }
             CK(cudaEventRecord(copy_done[s], cp));
         }
+        for (uint32_t j = count >= 2 ? count - 2 : 0; j < count; ++j) finalize(j);
         CK(cudaStreamSynchronize(st));
         CK(cudaStreamSynchronize(cp));
+        drain();
     } catch (...) {
         level_target_ = nullptr;
+        cudaStreamSynchronize(st);
         cudaStreamSynchronize(cp);
+        drain();
         cudaStreamDestroy(cp);
         for (int i = 0; i < 2; ++i) {
             cudaEventDestroy(kern_done[i]);

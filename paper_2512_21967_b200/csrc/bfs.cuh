@@ -8,6 +8,9 @@
 
 #include "bvss.cuh"
 #include "sigma.cuh"
+#include "xfer.cuh"
+
+#include <memory>
 
 namespace blestgpu {
 
@@ -64,8 +67,10 @@ public:
     BfsOutcome finish(uint32_t* levels_host);
     // BFS from each of `count` sources back to back, pipelined: source k's level array is
     // copied to levels_host + k·n (when non-null) on a copy stream while source k+1 runs
-    // (two device level buffers); each kernel's trace is folded on the device into a
-    // per-source summary. Returns per-source outcomes without per-level rows (trace empty).
+    // (two device level buffers) — narrowed to 1 or 2 bytes per vertex on the device and
+    // widened back to u32 by host threads (xfer.cuh; BLEST_D2H_PACK=0: plain u32 copies);
+    // each kernel's trace is folded on the device into a per-source summary. Returns
+    // per-source outcomes without per-level rows (trace empty).
     std::vector<BfsOutcome> run_batch(const uint32_t* srcs, uint32_t count, const EngineOptions& opt,
                                       uint32_t* levels_host);
     // level array written by the last launch (run_batch alternates two buffers)
@@ -78,6 +83,7 @@ public:
 
 private:
     void ensure_sigma();
+    void ensure_xfer();  // run_batch's narrow level transfers: device pack buffers, pinned ring, pool
     const DeviceBvss& b_;
     uint64_t words_ = 0, wstride_ = 0;
     uint32_t trace_cap_ = 0;
@@ -99,6 +105,13 @@ private:
     DevBuf<unsigned long long> trace_;   // trace_cap_ * 8
     DevBuf<unsigned long long> tstamp_;  // trace_cap_ * 3
     unsigned long long* pinned_ = nullptr;  // host mirror for ctl_ readback
+    // run_batch narrow transfers (xfer.cuh): packed levels on the device (2 buffers of up to
+    // 2 bytes per vertex), a pinned staging ring, per-slot max levels, host widening threads
+    static constexpr int kStageRing = 3;
+    DevBuf<uint8_t> dpack_;
+    uint8_t* stage_ = nullptr;
+    unsigned long long* stage_max_ = nullptr;
+    std::unique_ptr<WidenPool> pool_;
     uint32_t last_ctas_ = 0, last_threads_ = 0, last_src_ = 0;
     Mode last_mode_ = Mode::Eager;
     bool launched_ = false;

@@ -307,6 +307,40 @@ def test_run_batch_pipelined(oracle):
         B.run_batch(b, [0, g.num_vertices()], B.EngineMode.Lazy)
 
 
+def test_run_batch_narrow_transfers(oracle, monkeypatch):
+    """blest_bfs_batch's narrow level transfers (xfer.cuh): u8 while the deepest level fits,
+    u16 after a source overflows it, plain u32 after that — every source's u32 array equal to
+    the oracle's and to the plain-copy path (BLEST_D2H_PACK=0), unreached vertices included."""
+    g = B.Graph.generate_rmat(15, 16, 5)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    b = B.build_bvss(g)
+    srcs = g.pick_sources(7, 9)
+    want, _ = oracle.reference_bfs_many(csr, srcs)
+    assert (want == INF).any()  # RMAT leaves vertices unreached: the 0 -> kInf mapping is hit
+    lv, _ = B.run_batch(b, srcs, B.EngineMode.Lazy)
+    assert np.array_equal(lv, want)
+    # a path of 70 000 vertices (levels past 255 and past 65535) plus a separate triangle
+    n_path = 70_000
+    e = [(i, i + 1) for i in range(n_path - 1)] + [(n_path, n_path + 1), (n_path + 1, n_path + 2), (n_path + 2, n_path)]
+    n = n_path + 3 + 29  # + isolated vertices
+    g2 = B.Graph.from_edges(n, e, directed=False)
+    off2, tgt2 = g2.csr()
+    csr2 = oracle.Csr(n, off2, tgt2)
+    b2 = B.build_bvss(g2)
+    # mid: u8 overflows (-> u16); mid again: u16; 0: u16 overflows (-> u32); triangle: u32 path
+    srcs2 = np.array([n_path // 2, n_path // 2 + 7, 0, n_path + 1, 5], np.uint32)
+    want2, _ = oracle.reference_bfs_many(csr2, srcs2)
+    for pack in ("1", "0"):
+        monkeypatch.setenv("BLEST_D2H_PACK", pack)
+        lv2, cnts = B.run_batch(b2, srcs2, B.EngineMode.Eager)
+        assert np.array_equal(lv2, want2), pack
+        assert [c.levels_processed for c in cnts] == [int(w[w != INF].max()) for w in want2]
+    monkeypatch.setenv("BLEST_D2H_PACK", "1")
+    lv3, _ = B.run_batch(b2, srcs2[3:], B.EngineMode.Eager)  # triangle first: u8 all the way
+    assert np.array_equal(lv3, want2[3:])
+
+
 @pytest.mark.parametrize("kind", ["urand", "grid"])
 def test_auto_pipeline_non_social(oracle, kind):
     """C3 / C4 graph kinds at small scale through the whole pipeline (GPU generator →
