@@ -603,7 +603,8 @@ def main():
     E = np.array([c["E"] for c in census], np.float64)
     hm = len(t) / float(np.sum(t / E)) / 1e9
     total_s = float(t.sum())
-    balg = np.array([b_alg(n, c["D"], c["P"], c["V"], c["L"], lazy) for c in census], np.float64)
+    balg = np.array([b_alg(n, c["D"] - c["U"], c["P"], c["V"], c["L"] - (1 if c["U"] else 0), lazy)
+                     for c in census], np.float64)
     achieved = float(np.sum(balg) / total_s / 1e9)
     peak, peak_kind = load_peaks()
     value, elapsed = hm, total_s
@@ -699,12 +700,14 @@ def main():
                           frac=round(achieved / peak, 4), traffic=traffic,
                           peak_source=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
                           algorithmic_bytes_per_bfs=int(np.mean(balg)),
-                          formula="648 D + 4 P + 4 n + 4 V + k (n/8) L (SURVEY 8(d))"),
+                          formula="648 D + 4 P + 4 n + 4 V + k (n/8) L (SURVEY 8(d)); D and L without a "
+                                  "barren last level the lazy engine did not pull (detail.mean_unpulled)"),
             cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches), parity=parity,
             clocks=clk.summary(),
             detail=dict(grid=[g_ctas.value, g_thr.value], hm_gteps_rank0=round(hm, 4), mean_ms=round(1e3 * float(t.mean()), 4),
                         min_ms=round(1e3 * float(t.min()), 4), max_ms=round(1e3 * float(t.max()), 4),
                         mean_dequeues=int(np.mean([c["D"] for c in census])),
+                        mean_unpulled=int(np.mean([c["U"] for c in census])),
                         mean_levels=float(np.mean([c["L"] for c in census])),
                         mean_traversed_edges=int(E.mean()), arcs_per_s_G=round(2 * hm, 4)))
         print(json.dumps(line), flush=True)
@@ -910,9 +913,14 @@ def census_of(lib, L, b, prep, sources, lazy, pull, threads=0, grid_ctas=0, keep
         L.check(lib.blest_bfs(b.handle, int(s), C.byref(ecfg), lv.ctypes.data if lv is not None else None,
                               C.byref(ctr), None, 0))
         L.check(lib.blest_bfs_levels_device(b.handle, C.byref(lv_ptr)))
+        unp = C.c_uint64(0)
+        if hasattr(lib, "blest_bfs_last_unpulled"):  # absent only in an older BLEST_LIB experiment build
+            L.check(lib.blest_bfs_last_unpulled(b.handle, C.byref(unp)))
         e = prep["gp"].traversed_edges(lv_ptr.value)
-        out.append(dict(D=ctr.vss_dequeues, P=ctr.queue_pushes, V=ctr.visited_count, L=ctr.trace_len, E=e,
-                        levels=lv))
+        # roofline bytes count the VSSs actually pulled: a barren last level the lazy engine
+        # proved barren (every vertex with an in-edge visited) is in D but was never streamed
+        out.append(dict(D=ctr.vss_dequeues, U=int(unp.value), P=ctr.queue_pushes, V=ctr.visited_count,
+                        L=ctr.trace_len, E=e, levels=lv))
     return out
 
 

@@ -222,6 +222,11 @@ int blest_bfs_prepare(blest_bvss b, const blest_engine_config* cfg, uint64_t* en
 int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
 /* Launch geometry of the last run (CTAs, threads per CTA). */
 int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads);
+/* VSSs of the last finished blest_bfs / blest_bfs_finish run that the counters include but
+ * the kernel did not pull: the lazy engine stops pulling once every vertex with an in-edge
+ * is visited (the remaining level is provably barren; its trace row is written as the
+ * reference's would be). Measurement only (bytes actually streamed); no reference counterpart. */
+int blest_bfs_last_unpulled(blest_bvss b, uint64_t* vss);
 
 /* ---- tile known-answer entry (R:src/tc_emu.cpp:9-45) -------------------------------- */
 /* One warp per tile runs the engines' b1 pull (2 x mma.sync.m8n8k128.b1.and.popc with

@@ -152,6 +152,7 @@ SIGNATURES = {
     "blest_bfs_levels_device": (i32, [vp, P(vp)]),
     "blest_bfs_phase_times": (i32, [vp, vp, u32, P(u32)]),
     "blest_bfs_last_geometry": (i32, [vp, P(u32), P(u32)]),
+    "blest_bfs_last_unpulled": (i32, [vp, P(u64)]),
     "blest_bvss_build_rows": (i32, [vp, u32, u32, P(vp)]),
     "blest_partition_rows": (i32, [vp, u32, vp, vp]),
     "blest_rows_create": (i32, [vp, u32, u32, vp, P(vp)]),
@@ -188,6 +189,8 @@ def lib():
                 build()
             L = C.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
+                if os.environ.get("BLEST_LIB") and not hasattr(L, name):
+                    continue  # an experiment build (BLEST_LIB) from an older tree may lack newer entries
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args

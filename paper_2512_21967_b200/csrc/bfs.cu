@@ -82,7 +82,56 @@ __global__ void k_summarise(const unsigned long long* __restrict__ ctl, const un
     }
 }
 
+// Rows present in the BVSS (a slot with a nonzero mask byte), as a bitmap over original
+// ids: the vertices a BFS can discover (lazy exhaustion exit). Test-then-RED per slot.
+__global__ void k_present(const uint32_t* __restrict__ masks, const uint4* __restrict__ rows4, uint64_t lanes,
+                          uint32_t* present) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lanes; i += stride) {
+        const uint32_t mk = masks[i];
+        if (!mk) continue;
+        const uint4 r = rows4[i];
+        const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if ((mk >> (8 * c)) & 0xFFu) {
+                const uint32_t bit = 1u << (u[c] & 31);
+                if (!(present[u[c] >> 5] & bit)) atomicOr(&present[u[c] >> 5], bit);
+            }
+    }
+}
+
+__global__ void k_popc_sum(const uint32_t* __restrict__ w, uint64_t words, unsigned long long* out) {
+    unsigned long long c = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) c += __popc(w[i]);
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 }  // namespace
+
+void BfsEngine::ensure_present() {
+    if (present_built_) return;
+    present_.alloc(words_ ? words_ : 1);
+    cudaStream_t st = stream();
+    CK(cudaMemsetAsync(present_.p, 0, present_.bytes(), st));
+    const uint64_t lanes = 32ull * b_.num_vss;
+    if (lanes) {
+        k_present<<<grid_for(lanes, 256), 256, 0, st>>>(b_.masks.p, reinterpret_cast<const uint4*>(b_.row_ids.p),
+                                                        lanes, present_.p);
+        CK(cudaGetLastError());
+    }
+    DevBuf<unsigned long long> cnt(1);
+    CK(cudaMemsetAsync(cnt.p, 0, 8, st));
+    k_popc_sum<<<grid_for(words_ ? words_ : 1, 256), 256, 0, st>>>(present_.p, words_, cnt.p);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    present_rows_ = h;
+    present_built_ = true;
+}
 
 BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     words_ = ((uint64_t)b.n + 31) / 32;
@@ -100,7 +149,7 @@ BfsEngine::BfsEngine(const DeviceBvss& b) : b_(b) {
     bar_.alloc(4);  // count, pad, {payload | generation}
     trace_.alloc(8ull * trace_cap_);
     tstamp_.alloc(3ull * trace_cap_);
-    CK(cudaMallocHost(&pinned_, 8 * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&pinned_, 16 * sizeof(unsigned long long)));
 }
 
 BfsEngine::~BfsEngine() {
@@ -108,6 +157,12 @@ BfsEngine::~BfsEngine() {
     if (pinned_) cudaFreeHost(pinned_);
     if (stage_) cudaFreeHost(stage_);
     if (stage_max_) cudaFreeHost(stage_max_);
+}
+
+// Lazy exhaustion exit (bfs_lazy.cu), on unless BLEST_EXHAUST=0.
+static bool exhaust_enabled() {
+    const char* e = getenv("BLEST_EXHAUST");
+    return !(e && atoi(e) == 0);
 }
 
 // Widening threads: the CPUs this process may run on (bench.py pins it to the GPU's NUMA
@@ -153,11 +208,12 @@ void BfsEngine::ensure_sigma() {
 uint64_t BfsEngine::prepare(const EngineOptions& opt) {
     const char* sig_env = getenv("BLEST_SIGMA");
     if (opt.mode == Mode::Lazy && opt.sigma && !(sig_env && atoi(sig_env) == 0)) ensure_sigma();
+    if (opt.mode == Mode::Lazy && exhaust_enabled()) ensure_present();
     ensure_xfer();
     CK(cudaStreamSynchronize(stream()));
     uint64_t bytes = levels_.count * 4 + levels2_.count * 4 + dpack_.count + bits_.count * 4 + q_.count * 8 + ctl_.count * 8 +
                      agg_.count * 8 + aggS_.count * 8 + sl_.count * 8 + bar_.count * 4 + trace_.count * 8 +
-                     tstamp_.count * 8;
+                     tstamp_.count * 8 + present_.count * 4;
     if (sigma_on_)
         bytes += sigma_.rows.count * 4 + sigma_.sig.count * 4 + sigma_.inv.count * 4 + vext_.count * 4;
     return bytes;
@@ -224,6 +280,12 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
+    if (opt.mode == Mode::Lazy && !lazy_tma && exhaust_enabled()) {
+        ensure_present();
+        p.present = present_.p;
+        p.present_rows = present_rows_;
+    }
+    last_exhaust_ = p.present_rows != 0;
     if (sigma) {
         const uint64_t stride = sigma_.hot_words + wstride_;
         p.B0 = vext_.p;  // V_curr / V_next = [hot prefix | row words]
@@ -394,13 +456,15 @@ std::vector<BfsOutcome> BfsEngine::run_batch(const uint32_t* srcs, uint32_t coun
 BfsOutcome BfsEngine::finish(uint32_t* levels_host) {
     if (!launched_) throw LogicError("finish() without launch()");
     cudaStream_t st = stream();
-    CK(cudaMemcpyAsync(pinned_, ctl_.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pinned_, ctl_.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (levels_host && b_.n)
         CK(cudaMemcpyAsync(levels_host, levels_device(), (size_t)b_.n * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     BfsOutcome out;
     out.iterations = (uint32_t)pinned_[4];
     out.max_level = (uint32_t)pinned_[5];
+    out.unpulled_vss = last_exhaust_ ? pinned_[13] : 0;
+    last_unpulled_ = out.unpulled_vss;
     const bool runaway = pinned_[6] != 0;
     const uint32_t rows = std::min(out.iterations, trace_cap_);
     out.trace_truncated = out.iterations > trace_cap_;

@@ -46,6 +46,8 @@ struct BfsOutcome {
     std::vector<uint64_t> phase_ns;  // per level: start, stage-1 end (lazy), level end
     // totals over the levels (run_batch fills these instead of `trace`)
     uint64_t sum_queue = 0, sum_full = 0, sum_relaxed = 0, sum_pushes = 0;
+    // lazy: VSSs of a barren last level accounted without a pull (exhaustion exit), else 0
+    uint64_t unpulled_vss = 0;
 };
 
 // Per-structure device workspace; sized once, reused across sources.
@@ -79,11 +81,14 @@ public:
     uint32_t last_grid_ctas() const { return last_ctas_; }
     uint32_t last_threads() const { return last_threads_; }
     uint32_t last_src() const { return last_src_; }
+    // VSSs of the last finished run's barren level accounted without a pull (lazy exhaustion exit)
+    uint64_t last_unpulled() const { return last_unpulled_; }
     const DeviceBvss& bvss() const { return b_; }
 
 private:
     void ensure_sigma();
-    void ensure_xfer();  // run_batch's narrow level transfers: device pack buffers, pinned ring, pool
+    void ensure_xfer();
+    void ensure_present();  // lazy exhaustion exit: BVSS row bitmap + count  // run_batch's narrow level transfers: device pack buffers, pinned ring, pool
     const DeviceBvss& b_;
     uint64_t words_ = 0, wstride_ = 0;
     uint32_t trace_cap_ = 0;
@@ -112,6 +117,11 @@ private:
     uint8_t* stage_ = nullptr;
     unsigned long long* stage_max_ = nullptr;
     std::unique_ptr<WidenPool> pool_;
+    DevBuf<uint32_t> present_;  // rows present in the BVSS (original ids)
+    uint64_t present_rows_ = 0;
+    bool present_built_ = false;
+    bool last_exhaust_ = false;   // the last launch had the exhaustion exit armed
+    uint64_t last_unpulled_ = 0;
     uint32_t last_ctas_ = 0, last_threads_ = 0, last_src_ = 0;
     Mode last_mode_ = Mode::Eager;
     bool launched_ = false;

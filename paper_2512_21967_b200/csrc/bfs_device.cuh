@@ -54,6 +54,10 @@ struct Params {
     uint32_t lazy_recheck;  // lazy: test V_curr and re-check V_next at L2 (BLEST_LAZY_RECHECK)
     uint32_t tail_div;      // lazy: dense levels hand out their last 1/tail_div dynamically (0 = off)
     uint32_t log_cap;       // lazy: dirty-word log entries (in Q0) for the small stage 2 (0 = off)
+    // lazy exhaustion exit: rows present in the BVSS (bitmap, original ids) and their count;
+    // once 1 + Σ discovered covers every discoverable vertex the next level is barren
+    const uint32_t* __restrict__ present;
+    uint64_t present_rows;  // 0 = off
 };
 
 template <int THREADS, int MODE = 0>
@@ -308,7 +312,9 @@ template <int THREADS, int MODE>
 __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS, MODE>& sm, unsigned& gen,
                                                   uint32_t level, uint32_t (&c)[4], int stamp_slot,
                                                   const unsigned long long* payload = nullptr,
-                                                  unsigned long long* red_flag = nullptr) {
+                                                  unsigned long long* red_flag = nullptr,
+                                                  unsigned long long* vis_total = nullptr,
+                                                  unsigned long long* vis_out = nullptr) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t s = warp_sum(c[i]);
@@ -327,8 +333,10 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
     // red_flag: set (plain store, every writer stores 1) when the CTA issued a stage-1 RED;
     // read back as the payload after the barrier
     if (red_flag && threadIdx.x == 0 && mine[2]) *red_flag = 1ull;
+    // vis_total: running 1 + Σ discovered, added before the barrier, read back with the payload
+    if (vis_total && threadIdx.x == 0 && mine[0]) atomicAdd(vis_total, mine[0]);
     probe(p, level, 1u << 17, (uint32_t)mine[0], true);
-    const uint32_t pay = grid_barrier_pay(p.bar, gen, red_flag ? red_flag : payload);
+    const uint32_t pay = grid_barrier_pay(p.bar, gen, red_flag ? red_flag : payload, vis_total, vis_out);
     probe(p, level, 1u << 18, pay, true);
     if (threadIdx.x == 0) {
         const uint32_t row = min(level - 1, p.trace_cap - 1);

@@ -82,8 +82,17 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         p.ctl[0] = seed_e - seed_b;            // T: VSSs queued for the level
         p.ctl[1] = (seed_e > seed_b) ? 1 : 0;  // S: slice sets queued
         for (int i = 2; i < 16; ++i) p.ctl[i] = 0;
+        p.ctl[12] = 1;  // vertices visited so far (the source)
         for (int i = 0; i < 8; ++i) p.trace[i] = 0;
     }
+    // Exhaustion exit: a vertex can only be discovered through a BVSS row, so once the
+    // visited count reaches |rows ∪ {src}| no level can discover anything — the next level
+    // is the barren last one, and its trace row (queue = T, every other count 0) is known
+    // without pulling it (urand C3: the 2.2 M-VSS final level; BLEST_EXHAUST=0 disables).
+    const uint64_t reach = p.present_rows
+                               ? p.present_rows + (((p.present[src >> 5] >> (src & 31)) & 1u) ? 0u : 1u)
+                               : ~0ull;
+    unsigned long long visited = 1;
     uint32_t next_T = grid_barrier_pay(p.bar, gen, &p.ctl[0]);
     // The level array (4n bytes, the bulk of init_state) is written after the init barrier:
     // its stores drain while level 1's stage 1 runs (nothing reads L), and the barrier after
@@ -118,6 +127,18 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
             }
             if (level < p.trace_cap)
                 for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
+        }
+        if (visited >= reach) {  // barren by exhaustion (uniform: every thread read the same count)
+            if (gtid == 0) {
+                p.ctl[13] = len;  // VSSs accounted without a pull (bench: bytes actually streamed)
+                if (level - 1 < p.trace_cap) {
+                    const unsigned long long t = globaltimer();
+                    p.tstamp[3ull * (level - 1) + 1] = t;
+                    p.tstamp[3ull * (level - 1) + 2] = t;
+                }
+            }
+            ++level;  // the barren level counts as an iteration (R:src/bfs_engine.cpp:117-124)
+            break;
         }
         unsigned long long* Qc = p.Q0;
         // the level's frontier words (α) and the next level's: B2/B3 alternate, so the next
@@ -178,13 +199,13 @@ __global__ void __launch_bounds__(THREADS, BLEST_LAZY_MINB) k_bfs_lazy(Params p)
         if (prev_small) {
             small_stage2<THREADS, SIGMA>(p, level, ctr, Fn, reinterpret_cast<const uint32_t*>(p.Q0), s1,
                                          &p.ctl[8 + (level & 1)]);
-            next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[8 + (level & 1)]);
+            next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[8 + (level & 1)], nullptr, &p.ctl[12], &visited);
         } else {
             if (SIGMA)
                 lazy_stage2_hot<THREADS>(p, sm, level, ctr, gen, Fn);
             else
                 lazy_stage2<THREADS>(p, sm, level, ctr, Fn);
-            next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0]);
+            next_T = level_barrier(p, sm, gen, level, ctr, 2, &p.ctl[0], nullptr, &p.ctl[12], &visited);
         }
     }
     if (gtid == 0) p.ctl[4] = level - 1;

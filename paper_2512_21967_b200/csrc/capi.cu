@@ -774,6 +774,13 @@ int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels) {
     API_END
 }
 
+int blest_bfs_last_unpulled(blest_bvss b, uint64_t* vss) {
+    API_BEGIN
+    NEED(b && vss, "null argument");
+    *vss = b->eng().last_unpulled();
+    API_END
+}
+
 int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads) {
     API_BEGIN
     NEED(b, "null bvss");

@@ -139,15 +139,24 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
 // 1.2 µs on B200 vs 2.4-3.3 µs for a count-reset-generation barrier (tools/probes/
 // barrier_probe.cu), so it is the primitive; `payload` (a value every CTA needs right after
 // the barrier, e.g. the next queue length) is then read once per CTA and broadcast.
-__device__ __forceinline__ uint32_t grid_barrier_pay(unsigned* bar, unsigned& gen, const unsigned long long* payload) {
+// payload2 (optional): a second word read with the first (same 128 B line in practice, so no
+// extra latency), returned through out2.
+__device__ __forceinline__ uint32_t grid_barrier_pay(unsigned* bar, unsigned& gen, const unsigned long long* payload,
+                                                     const unsigned long long* payload2 = nullptr,
+                                                     unsigned long long* out2 = nullptr) {
     (void)bar;
     __shared__ uint32_t s_pay;
+    __shared__ unsigned long long s_pay2;
     cooperative_groups::this_grid().sync();
     gen += 1;
-    if (!payload) return 0;
-    if (threadIdx.x == 0) s_pay = (uint32_t)ld_relaxed_gpu_u64(payload);
+    if (!payload && !payload2) return 0;
+    if (threadIdx.x == 0) {
+        if (payload) s_pay = (uint32_t)ld_relaxed_gpu_u64(payload);
+        if (payload2) s_pay2 = ld_relaxed_gpu_u64(payload2);
+    }
     __syncthreads();
-    return s_pay;
+    if (payload2) *out2 = s_pay2;
+    return payload ? s_pay : 0u;
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) { grid_barrier_pay(bar, gen, nullptr); }
