@@ -307,6 +307,45 @@ def test_run_batch_pipelined(oracle):
         B.run_batch(b, [0, g.num_vertices()], B.EngineMode.Lazy)
 
 
+@pytest.mark.parametrize("kind", ["urand", "grid", "rmat"])
+def test_lazy_exhaustion_exit(oracle, monkeypatch, kind):
+    """The lazy engine's exhaustion exit (bfs_lazy.cu): on a connected graph the barren last
+    level is accounted without a pull (blest_bfs_last_unpulled = its queue), and levels,
+    counters and the whole per-level trace still equal the reference engine's, with the exit
+    armed (BLEST_EXHAUST=1, default) and off; on RMAT it fires only if the source's component
+    holds every vertex with an edge."""
+    import ctypes as C
+    from paper_2512_21967_b200 import _lib as L
+    if kind == "urand":
+        g = B.Graph.generate_urand(1 << 14, 16 << 14, 5)
+    elif kind == "grid":
+        g = B.Graph.generate_grid(64, 96)
+    else:
+        g = B.Graph.generate_rmat(14, 16, 5)
+    off, tgt = g.csr()
+    csr = oracle.Csr(g.num_vertices(), off, tgt)
+    b = B.build_bvss(g)
+    ob = oracle.build_bvss(csr)
+    for src in g.pick_sources(3, 11):
+        src = int(src)
+        want = oracle.reference_bfs(csr, src)[0]
+        o_eng = oracle.run_engine(ob, src, True)
+        got = {}
+        for ex in ("1", "0"):
+            monkeypatch.setenv("BLEST_EXHAUST", ex)
+            res, cnt = run(b, src, "lazy", "popc")
+            unp = C.c_uint64(7)
+            L.check(L.lib().blest_bfs_last_unpulled(b.handle, C.byref(unp)))
+            assert np.array_equal(res.levels, want), (kind, src, ex)
+            assert cnt.vss_dequeues == o_eng.counters["vss_dequeues"]
+            assert np.array_equal(trace_cols(cnt)[:, [1, 3, 4]], o_eng.trace[:, [1, 3, 7]])
+            got[ex] = (int(unp.value), int(cnt.trace[-1].queue_size), int(cnt.trace[-1].discovered))
+        assert got["0"][0] == 0
+        assert got["1"][0] in (0, got["1"][1]) and (got["1"][0] == 0 or got["1"][2] == 0), got
+        if kind != "rmat":  # connected: the last level is barren and was not pulled
+            assert got["1"][0] > 0, got
+
+
 def test_run_batch_narrow_transfers(oracle, monkeypatch):
     """blest_bfs_batch's narrow level transfers (xfer.cuh): u8 while the deepest level fits,
     u16 after a source overflows it, plain u32 after that — every source's u32 array equal to
