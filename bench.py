@@ -459,7 +459,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunk", type=int, default=16, help="sources per blest_bfs_batch call in the e2e leg")
+    ap.add_argument("--e2e-chunk", type=int, default=64,
+                    help="sources per blest_bfs_batch call in the e2e leg (capped by a 4.4 GB host buffer)")
     ap.add_argument("--e2e-pageable", action="store_true",
                     help="e2e output in pageable (pre-touched) host memory instead of pinned")
     ap.add_argument("--validate", type=int, default=-1,
@@ -619,10 +620,11 @@ def main():
         elapsed = float(max(x[1].item() for x in allv))
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----
-    # blest_bfs_batch: the public many-sources call; source k's full level array is copied
-    # to pinned host memory while source k+1 runs. Chunks of <= 16 sources (one pinned
-    # buffer, reused; a 64-source / 4.3 GB buffer measured slower D2H: e2e 141 -> 74 GTEPS);
-    # each source's time = its chunk's wall time / size.
+    # blest_bfs_batch: the public many-sources call (the CLI's loop over its sources as one
+    # call); source k's level array crosses PCIe narrowed and is widened into the host buffer
+    # while source k+1 runs. One call for all sources up to a 4.4 GB host buffer (C2: 64, C5:
+    # 8; chunks of 16 measured 160 vs 169 GTEPS on C2 — each call ends with one exposed copy,
+    # profiles/r02_e2e_ab/); each source's time = its call's wall time / size.
     e2e = None
     if not args.no_e2e:
         chunk = max(1, min(args.e2e_chunk, len(mine), int(4.4e9 // (4 * max(n, 1)))))
