@@ -812,7 +812,7 @@ def run_partitioned(args, prep, B, L, lib, perm, world, rank, local, stream):
         res = results(True)
         t = e0.elapsed_time(e1) / 1e3
         e = sum(int(deg[r.row_lo:r.row_hi][r.levels != 0xFFFFFFFF].sum()) for r in res)
-        q = sum(r.queue for r in res)
+        q = sum(r.queue - r.unpulled for r in res)  # VSSs actually pulled (exhaustion exit)
         if world > 1 and not virtual:
             tt = torch.tensor([t, float(e), float(q)], dtype=torch.float64, device=coll_dev())
             tmax = tt.clone()

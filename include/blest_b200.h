@@ -258,6 +258,9 @@ typedef struct {
     uint64_t discovered;  /* owned rows discovered (source excluded) */
     uint64_t relaxed;     /* stage-1 REDs issued */
     uint64_t pushes;      /* local VSSs queued for next levels */
+    uint64_t unpulled;    /* local VSSs of a barren last level counted in queue but not pulled:
+                             every rank stops pulling once every vertex with an in-arc is
+                             visited (exhaustion exit; BLEST_EXHAUST=0 pulls it) */
 } blest_rows_stats;
 /* Row ranges balanced by BVSS slice count (one slice = a (column slice set, row) pair, the
  * unit of pull work): word_bounds[0..world], slices[0..world-1] (optional) per rank. */

@@ -98,7 +98,8 @@ class LevelTraceT(C.Structure):
 
 class RowsStatsT(C.Structure):
     _fields_ = [("iterations", C.c_uint32), ("max_level", C.c_uint32), ("queue", C.c_uint64),
-                ("discovered", C.c_uint64), ("relaxed", C.c_uint64), ("pushes", C.c_uint64)]
+                ("discovered", C.c_uint64), ("relaxed", C.c_uint64), ("pushes", C.c_uint64),
+                ("unpulled", C.c_uint64)]
 
 
 # Every symbol include/blest_b200.h declares, with its ctypes signature.

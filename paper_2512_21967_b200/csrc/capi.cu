@@ -442,6 +442,7 @@ int blest_bvss_build_rows(blest_graph g, uint32_t row_lo, uint32_t row_hi, blest
 
 struct blest_rows_s {
     DeviceBvss b;
+    DevBuf<uint32_t> present;  // rows present in the whole BVSS (exhaustion exit)
     std::unique_ptr<RowsEngine> e;
 };
 
@@ -469,6 +470,8 @@ int blest_rows_create(blest_graph g, uint32_t rank, uint32_t world, const uint64
     const uint64_t lo = std::min<uint64_t>(32 * bounds[rank], g->g.n), hi = std::min<uint64_t>(32 * bounds[rank + 1], g->g.n);
     h->b = bvss_build(g->g, (uint32_t)lo, (uint32_t)hi);
     h->e = std::make_unique<RowsEngine>(h->b, rank, world, bounds);
+    const uint64_t present_rows = graph_present_rows(g->g, h->present);
+    h->e->set_present(h->present.p, present_rows);
     *out = h.release();
     API_END
 }
@@ -565,6 +568,7 @@ int blest_rows_finish(blest_rows r, uint32_t* levels_owned, blest_rows_stats* ou
         out->discovered = s.discovered;
         out->relaxed = s.relaxed;
         out->pushes = s.pushes;
+        out->unpulled = s.unpulled;
     }
     API_END
 }

@@ -25,6 +25,8 @@ enum : int {
     kStatus = 6,   // 0 ok, 1 runaway, 2 cross-rank barrier timeout
     kXBar = 7,     // fused: cross-rank barriers passed (persistent across BFSs)
     kDone = 8,     // stepped: BFS finished (later launches are no-ops)
+    kVis = 9,      // stepped: vertices visited through the previous level (9 | 10 by level parity)
+    kUnpulled = 11,  // local VSSs of a barren last level accounted without a pull (exhaustion exit)
     kCtl = 16
 };
 
@@ -58,6 +60,10 @@ struct RowsParams {
     const uint32_t* sig;
     uint32_t* H;
     unsigned* hflags;          // mapped host flags
+    // exhaustion exit (as in the lazy kernel): global bitmap of the rows present in the BVSS
+    // (every vertex with an in-arc) and their count; 0 = off
+    const uint32_t* present;
+    uint64_t present_rows;
 };
 
 // Every rank's parameters of one launch, passed by value (kernel parameter space: constant
@@ -462,6 +468,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
             p.ctl[kIters] = 0;
             p.ctl[kStatus] = 0;
             p.ctl[kDone] = 0;
+            p.ctl[kUnpulled] = 0;
             for (int i = 0; i < 8; ++i) p.trace[i] = 0;
         }
         grid_sync();
@@ -495,10 +502,24 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
         const uint64_t cs = (uint64_t)(p.src >> 5) / CH;
         if (cs >= k0 && cs < k1) prev_nz = chunk_bit(cs - k0);
     }
+    // exhaustion exit: every rank sees the same exchanged frontiers, so every rank keeps the
+    // same visited count (1 + Σ kBits) and stops at the same level once it covers every row
+    // present anywhere (plus the source if it is not one): that level is barren
+    const uint64_t reach = p.present_rows
+                               ? p.present_rows + (((p.present[p.src >> 5] >> (p.src & 31)) & 1u) ? 0u : 1u)
+                               : ~0ull;
+    unsigned long long visited = 0;  // fused: running sum of kBits (level 1: the source)
     for (;; ++level) {
         const unsigned long long len = ld_relaxed_gpu_u64(&p.ctl[kT]);
         const uint32_t S = (uint32_t)ld_relaxed_gpu_u64(&p.ctl[kS]);
-        if (!STEPPED && ld_relaxed_gpu_u64(&p.ctl[kBits]) == 0) break;
+        const unsigned long long bits = ld_relaxed_gpu_u64(&p.ctl[kBits]);
+        if (!STEPPED && bits == 0) break;
+        if (STEPPED) {  // one launch per level: the count travels in ctl (two slots by parity)
+            visited = (level == 1 ? 0ull : ld_relaxed_gpu_u64(&p.ctl[kVis + (level & 1)])) + bits;
+            if (gtid == 0) p.ctl[kVis + ((level + 1) & 1)] = visited;
+        } else {
+            visited += bits;
+        }
         if (level > p.cap) {  // runaway (R:src/bfs_engine.cpp:72-75)
             if (gtid == 0) {
                 p.ctl[kStatus] = 1;
@@ -522,6 +543,20 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_bfs_rows(const __gr
             }
             if (level < p.trace_cap)
                 for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
+        }
+        if (visited >= reach) {  // barren by exhaustion: its trace row is (level, len, 0, …)
+            if (gtid == 0) {
+                p.ctl[kUnpulled] = len;
+                if (STEPPED) {
+                    p.ctl[kIters] = level;
+                    p.ctl[kDone] = 1;
+                    __threadfence_system();
+                    p.hflags[1] = level;
+                }
+            }
+            if (STEPPED) return;
+            ++level;  // the barren level counts as an iteration
+            break;
         }
         // ---- stage 1: pull of the local VSSs (lazy_pull.cuh) ----
         // reconverge warp 0 after the single-thread blocks above: a diverged warp would run
@@ -645,6 +680,41 @@ __global__ void k_word_slices(const uint32_t* __restrict__ cnt, uint32_t n, uint
 }
 
 }  // namespace
+
+namespace {
+__global__ void k_arc_targets(const uint32_t* __restrict__ tgt, uint64_t m, uint32_t* present) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = tgt[i], bit = 1u << (r & 31);
+        if (!(present[r >> 5] & bit)) atomicOr(&present[r >> 5], bit);
+    }
+}
+__global__ void k_popc_words(const uint32_t* __restrict__ w, uint64_t words, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        c += __popc(w[i]);
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+}  // namespace
+
+uint64_t graph_present_rows(const DeviceGraph& g, DevBuf<uint32_t>& bits) {
+    const uint64_t words = ((uint64_t)g.n + 31) / 32;
+    bits.alloc(words ? words : 1);
+    cudaStream_t st = stream();
+    CK(cudaMemsetAsync(bits.p, 0, bits.bytes(), st));
+    if (g.m) {
+        k_arc_targets<<<grid_for(g.m, 256), 256, 0, st>>>(g.tgt.p, g.m, bits.p);
+        CK(cudaGetLastError());
+    }
+    DevBuf<unsigned long long> cnt(1);
+    CK(cudaMemsetAsync(cnt.p, 0, 8, st));
+    k_popc_words<<<grid_for(words ? words : 1, 256), 256, 0, st>>>(bits.p, words, cnt.p);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return h;
+}
 
 std::vector<uint64_t> partition_rows_by_slices(const DeviceGraph& g, uint32_t world, std::vector<uint64_t>* slices_out) {
     if (world == 0) throw InvalidArgument("world size must be positive");
@@ -832,6 +902,11 @@ void RowsEngine::fill_params(RowsParams& p, uint32_t src, uint32_t level, const 
     p.tstamp = tstamp_.p;
     p.hflags = hflags_dev_;
     p.sys_scope = opened_.empty() ? 0u : 1u;
+    const char* ex = getenv("BLEST_EXHAUST");
+    if (present_ && !(ex && atoi(ex) == 0)) {
+        p.present = present_;
+        p.present_rows = present_rows_;
+    }
     if (const char* x = getenv("BLEST_XSTAMP")) p.xstamp = (uint32_t)atoi(x);
 }
 
@@ -945,6 +1020,7 @@ RowsEngine::Stats RowsEngine::finish(uint32_t* levels_owned_host) {
     CK(cudaStreamSynchronize(st));
     Stats s;
     s.iterations = (uint32_t)c[kIters];
+    s.unpulled = c[kUnpulled];
     if (c[kStatus] == 1) throw RuntimeError("BFS ran past the level safety cap — engine invariant broken");
     if (c[kStatus] == 2) throw RuntimeError("rows engine: cross-rank barrier timed out (a peer is not running)");
     const uint32_t rows = std::min(s.iterations, trace_cap_);

@@ -63,6 +63,7 @@ public:
     struct Stats {
         uint32_t iterations = 0, max_level = 0;
         uint64_t queue = 0, discovered = 0, relaxed = 0, pushes = 0;
+        uint64_t unpulled = 0;  // local VSSs of a barren last level not pulled (exhaustion exit)
     };
     Stats finish(uint32_t* levels_owned_host);
     // per level of the last BFS (rank 0's timeline in a group launch, %globaltimer ns):
@@ -73,11 +74,16 @@ public:
     uint32_t rank() const { return rank_; }
     uint32_t world() const { return world_; }
     const DeviceBvss& bvss() const { return b_; }
+    // exhaustion exit: global bitmap of the rows present in the whole BVSS (device, n bits,
+    // owned by the caller) and their count (graph_present_rows); unset = off
+    void set_present(const uint32_t* bits, uint64_t count) { present_ = bits; present_rows_ = count; }
     // device copy of this rank's kernel parameters (group launch)
     void fill_params(RowsParams& p, uint32_t src, uint32_t level, const uint32_t* recv, bool allow_sigma = true) const;
 
 private:
     const DeviceBvss& b_;
+    const uint32_t* present_ = nullptr;
+    uint64_t present_rows_ = 0;
     uint32_t rank_, world_;
     uint32_t row_lo_, row_hi_;
     uint64_t words_, w_lo_, w_hi_, per_, xstride_;
@@ -107,5 +113,7 @@ void rows_group_launch(const std::vector<RowsEngine*>& ranks, uint32_t src);
 // Row ranges balanced by BVSS slice count: bounds[0..world] in frontier words (32 rows),
 // bounds[0] = 0, bounds[world] = ⌈n/32⌉. slices_out (optional, host) gets each rank's count.
 std::vector<uint64_t> partition_rows_by_slices(const DeviceGraph& g, uint32_t world, std::vector<uint64_t>* slices_out);
+// Rows present in the BVSS of g (every vertex with an in-arc) as a bitmap (n bits) + count.
+uint64_t graph_present_rows(const DeviceGraph& g, DevBuf<uint32_t>& bits);
 
 }  // namespace blestgpu

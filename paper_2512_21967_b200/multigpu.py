@@ -66,6 +66,7 @@ class RowsResult:
     discovered: int     # owned rows discovered (source excluded)
     queue: int          # Σ local VSS queue over the levels
     collectives: int = 0
+    unpulled: int = 0   # local VSSs of a barren last level counted in queue, not pulled (exhaustion exit)
 
 
 class _DevArray:
@@ -149,7 +150,7 @@ class RowsEngine:
         st = L.RowsStatsT()
         L.check(L.lib().blest_rows_finish(self._h, out.ctypes.data if levels else None, C.byref(st)))
         return RowsResult(out[: self.row_hi - self.row_lo] if levels else None, self.row_lo, self.row_hi,
-                          st.iterations, st.discovered, st.queue)
+                          st.iterations, st.discovered, st.queue, unpulled=st.unpulled)
 
 
 def set_local_peers(engines: list[RowsEngine]):

@@ -128,6 +128,45 @@ def test_fused_matches_single_gpu_lazy_counters(oracle):
         assert r.queue == cnt.vss_dequeues
 
 
+@pytest.mark.parametrize("kind", ["urand", "grid"])
+def test_rows_exhaustion_exit(oracle, monkeypatch, kind):
+    """Connected graphs: every rank stops pulling at the same barren last level (exhaustion
+    exit), levels stay bit-exact, the iteration count equals the single-GPU lazy engine's,
+    and one rank's queue / unpulled equal the lazy engine's dequeues / unpulled VSSs; fused
+    (1, 3, 8 virtual ranks) and stepped (2 ranks), exit armed and off."""
+    if kind == "urand":
+        g = B.Graph.generate_urand(1 << 13, 16 << 13, 7)
+    else:
+        g = B.apply_permutation(B.Graph.generate_grid(40, 52), B.relabel_permutation(40 * 52, 3))
+    n = g.num_vertices()
+    off, tgt = g.csr()
+    csr = oracle.Csr(n, off, tgt)
+    b = B.build_bvss(g)
+    for ex in ("1", "0"):
+        monkeypatch.setenv("BLEST_EXHAUST", ex)
+        for src in g.pick_sources(2, 5):
+            src = int(src)
+            want = oracle.reference_bfs(csr, src)[0]
+            res1, cnt1 = B.run_lazy(b, src, B.EngineConfig())
+            unp1 = C.c_uint64(0)
+            L.check(L.lib().blest_bfs_last_unpulled(b.handle, C.byref(unp1)))
+            assert (unp1.value > 0) == (ex == "1")
+            for world in (1, 3, 8):
+                engs = engines_for(g, world)
+                group_bfs(engs, src)
+                res = [e.finish() for e in engs]
+                assert np.array_equal(assemble(res, n), want), (kind, world, src, ex)
+                assert {r.iterations for r in res} == {len(cnt1.trace)}
+                assert (sum(r.unpulled for r in res) > 0) == (ex == "1")
+                if world == 1:
+                    assert res[0].queue == cnt1.vss_dequeues and res[0].unpulled == unp1.value
+            bounds, _ = partition_rows(g, 2)
+            engs = [RowsEngine(g, r, 2, bounds) for r in range(2)]
+            res = run_stepped_local(engs, src)
+            assert np.array_equal(assemble(res, n), want), (kind, "stepped", src, ex)
+            assert {r.iterations for r in res} == {len(cnt1.trace)}
+
+
 def test_errors():
     g = B.Graph.generate_rmat(8, 8, 1)
     bounds, _ = partition_rows(g, 2)
