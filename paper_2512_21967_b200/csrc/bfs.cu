@@ -178,7 +178,7 @@ static int xfer_threads() {
 void BfsEngine::ensure_xfer() {
     if (!levels2_.p) levels2_.alloc(b_.n ? b_.n : 1);
     if (stage_ || !b_.n) return;
-    const uint64_t slot = 2ull * b_.n;
+    const uint64_t slot = xfer_slot_bytes(b_.n);
     dpack_.alloc(2 * slot);
     CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_), kStageRing * slot, cudaHostAllocDefault));
     CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_max_), kStageRing * sizeof(unsigned long long),
@@ -344,7 +344,7 @@ std::vector<BfsOutcome> BfsEngine::run_batch(const uint32_t* srcs, uint32_t coun
         CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
     }
     uint32_t* bufs[2] = {levels_.p, levels2_.p};
-    const uint64_t slot = 2 * n;
+    const uint64_t slot = xfer_slot_bytes(n);
     int width = 1;
     std::vector<int> wk(count, 0);  // transfer width of source k (0 = u32 copy)
     std::vector<WidenPool::Job> jobs(count);

@@ -21,6 +21,10 @@
 
 namespace blestgpu {
 
+// Bytes per packed buffer (2 per vertex at most), rounded to 16 so every buffer of a
+// back-to-back pair keeps the pack kernel's 4 B / 8 B vector stores aligned (odd n).
+inline uint64_t xfer_slot_bytes(uint64_t n) { return (2 * n + 15) & ~15ull; }
+
 // levels (u32, n) -> out (width 1 or 2 bytes per vertex): (level + 1) truncated, 0 for kInf.
 void pack_levels(const uint32_t* levels, uint64_t n, int width, void* out, cudaStream_t st);
 

@@ -362,7 +362,7 @@ def test_run_batch_narrow_transfers(oracle, monkeypatch):
     # a path of 70 000 vertices (levels past 255 and past 65535) plus a separate triangle
     n_path = 70_000
     e = [(i, i + 1) for i in range(n_path - 1)] + [(n_path, n_path + 1), (n_path + 1, n_path + 2), (n_path + 2, n_path)]
-    n = n_path + 3 + 29  # + isolated vertices
+    n = n_path + 3 + 30  # + isolated vertices; odd n (the second pack buffer's alignment)
     g2 = B.Graph.from_edges(n, e, directed=False)
     off2, tgt2 = g2.csr()
     csr2 = oracle.Csr(n, off2, tgt2)
