@@ -215,8 +215,10 @@ int blest_bfs_finish(blest_bvss b, uint32_t* levels_out, blest_counters* counter
  * level start, lazy stage-1 end, level end); *rows = levels recorded. */
 int blest_bfs_phase_times(blest_bvss b, uint64_t* out, uint32_t cap, uint32_t* rows);
 /* Build what runs of `cfg` need before the first BFS (lazy: the hot-row view of the visited
- * bitmaps) and report the engine's device bytes (workspace + view); optional — the first
- * BFS builds it otherwise. No reference counterpart (device workspace). */
+ * bitmaps and the present-row bitmap of the exhaustion exit; every mode: the second level
+ * buffer, the packed-level buffers, the pinned staging ring (3 × 2n bytes) and the widening
+ * threads of blest_bfs_batch) and report the engine's device bytes; optional — the first
+ * BFS / batch builds them otherwise. No reference counterpart (device workspace). */
 int blest_bfs_prepare(blest_bvss b, const blest_engine_config* cfg, uint64_t* engine_bytes);
 /* Device pointer to the level array of the last run on b (n entries). */
 int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
