@@ -208,7 +208,7 @@ void BfsEngine::ensure_sigma() {
 uint64_t BfsEngine::prepare(const EngineOptions& opt) {
     const char* sig_env = getenv("BLEST_SIGMA");
     if (opt.mode == Mode::Lazy && opt.sigma && !(sig_env && atoi(sig_env) == 0)) ensure_sigma();
-    if (opt.mode == Mode::Lazy && exhaust_enabled()) ensure_present();
+    if (exhaust_enabled()) ensure_present();
     ensure_xfer();
     CK(cudaStreamSynchronize(stream()));
     uint64_t bytes = levels_.count * 4 + levels2_.count * 4 + dpack_.count + bits_.count * 4 + q_.count * 8 + ctl_.count * 8 +
@@ -280,7 +280,7 @@ void BfsEngine::launch(uint32_t src, const EngineOptions& opt) {
     p.src = src;
     p.cap = opt.max_levels ? opt.max_levels : b_.n + 1;
     p.num_warps = opt.num_warps;
-    if (opt.mode == Mode::Lazy && !lazy_tma && exhaust_enabled()) {
+    if (!lazy_tma && exhaust_enabled()) {  // both engines (the TMA ablation has no exit)
         ensure_present();
         p.present = present_.p;
         p.present_rows = present_rows_;

@@ -314,7 +314,8 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
                                                   const unsigned long long* payload = nullptr,
                                                   unsigned long long* red_flag = nullptr,
                                                   unsigned long long* vis_total = nullptr,
-                                                  unsigned long long* vis_out = nullptr) {
+                                                  unsigned long long* vis_out = nullptr,
+                                                  bool disc_before = false) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t s = warp_sum(c[i]);
@@ -335,6 +336,10 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
     if (red_flag && threadIdx.x == 0 && mine[2]) *red_flag = 1ull;
     // vis_total: running 1 + Σ discovered, added before the barrier, read back with the payload
     if (vis_total && threadIdx.x == 0 && mine[0]) atomicAdd(vis_total, mine[0]);
+    // disc_before (eager exhaustion exit, dense levels): the trace row's discoveries are
+    // added before the barrier, so the row is final once the barrier is passed
+    if (disc_before && threadIdx.x == 0 && mine[0])
+        atomicAdd(&p.trace[8ull * min(level - 1, p.trace_cap - 1) + 3], mine[0]);
     probe(p, level, 1u << 17, (uint32_t)mine[0], true);
     const uint32_t pay = grid_barrier_pay(p.bar, gen, red_flag ? red_flag : payload, vis_total, vis_out);
     probe(p, level, 1u << 18, pay, true);
@@ -342,7 +347,7 @@ __device__ __forceinline__ uint32_t level_barrier(const Params& p, Smem<THREADS,
         const uint32_t row = min(level - 1, p.trace_cap - 1);
         unsigned long long* t = p.trace + 8ull * row;
         if (mine[0]) {
-            atomicAdd(&t[3], mine[0]);
+            if (!disc_before) atomicAdd(&t[3], mine[0]);
             atomicMax(&p.ctl[5], (unsigned long long)level);
         }
         if (mine[1]) atomicAdd(&t[4], mine[1]);

@@ -79,7 +79,22 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
         p.ctl[0] = 0;
         p.ctl[1] = seed_e - seed_b;
         for (int i = 2; i < 8; ++i) p.ctl[i] = 0;
+        p.ctl[13] = 0;  // VSSs of a barren level accounted without a pull
         for (int i = 0; i < 8; ++i) p.trace[i] = 0;
+    }
+    // Exhaustion exit (as in the lazy kernel): the next level is barren once 1 + Σ discovered
+    // reaches |BVSS rows ∪ {src}|. Nothing is added to a sparse level (C4 runs 8.6 K of them;
+    // reading the trace rows at every barrier cost it 8 %): after a DENSE level, whose CTAs
+    // add their discoveries to its trace row before the barrier, thread 0 of every CTA sums
+    // the trace rows not summed yet — all final then — so the count is exact after a dense
+    // level and stale (low: never an early exit) after a sparse one.
+    // (state in shared memory: registers are what this kernel is short of)
+    __shared__ unsigned long long s_vis, s_reach;  // 1 + Σ discovered of trace rows [0, s_summed)
+    __shared__ uint32_t s_summed;
+    if (threadIdx.x == 0) {
+        s_reach = p.present_rows ? p.present_rows + (((p.present[src >> 5] >> (src & 31)) & 1u) ? 0u : 1u) : ~0ull;
+        s_vis = 1;
+        s_summed = 0;
     }
     uint32_t next_len = grid_barrier_pay(p.bar, gen, &p.ctl[1]);
 
@@ -106,6 +121,18 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
             }
             if (level < p.trace_cap)
                 for (int i = 0; i < 8; ++i) p.trace[8ull * level + i] = 0;
+        }
+        if (s_vis >= s_reach) {  // barren by exhaustion (uniform: every CTA read the same rows)
+            if (gtid == 0) {
+                p.ctl[13] = len;
+                if (level - 1 < p.trace_cap) {
+                    const unsigned long long t = globaltimer();
+                    p.tstamp[3ull * (level - 1) + 1] = t;
+                    p.tstamp[3ull * (level - 1) + 2] = t;
+                }
+            }
+            ++level;  // the barren level counts as an iteration (R:src/bfs_engine.cpp:117-124)
+            break;
         }
         // triple buffers by select (a runtime-indexed array would live in local memory)
         auto qsel = [&](uint32_t k) { return k == 0 ? p.Q0 : (k == 1 ? p.Q1 : p.Q2); };
@@ -242,7 +269,17 @@ __global__ void __launch_bounds__(THREADS, BLEST_EAGER_MINB) k_bfs_eager(Params 
             atomicMax(&p.tstamp[3ull * (level - 1) + 1], globaltimer());
         if ((p.xflags & 64) && threadIdx.x == 0 && level - 1 < p.trace_cap)  // timing study:
             atomicMax(&p.tstamp[3ull * (level - 1) + 1], globaltimer());      // last CTA's pull end
-        next_len = level_barrier(p, sm, gen, level, ctr, 2, qlen_next);
+        const bool track = p.present_rows && recheck && level < p.trace_cap;  // row level-1 not clamped
+        next_len = level_barrier(p, sm, gen, level, ctr, 2, qlen_next, nullptr, nullptr, nullptr, track);
+        if (track) {  // uniform: rows [s_summed, level) are final now
+            if (threadIdx.x == 0) {
+                unsigned long long add = 0;
+                for (uint32_t k = s_summed; k < level; ++k) add += ld_relaxed_gpu_u64(&p.trace[8ull * k + 3]);
+                s_vis += add;
+                s_summed = level;
+            }
+            __syncthreads();
+        }
     }
     if (gtid == 0) p.ctl[4] = level - 1;
 }

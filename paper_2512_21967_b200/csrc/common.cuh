@@ -141,6 +141,8 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
 // the barrier, e.g. the next queue length) is then read once per CTA and broadcast.
 // payload2 (optional): a second word read with the first (same 128 B line in practice, so no
 // extra latency), returned through out2.
+// payload2 (optional): a second word read with the first (same 128 B line in practice, so no
+// extra latency), returned through out2.
 __device__ __forceinline__ uint32_t grid_barrier_pay(unsigned* bar, unsigned& gen, const unsigned long long* payload,
                                                      const unsigned long long* payload2 = nullptr,
                                                      unsigned long long* out2 = nullptr) {

@@ -307,10 +307,12 @@ def test_run_batch_pipelined(oracle):
         B.run_batch(b, [0, g.num_vertices()], B.EngineMode.Lazy)
 
 
+@pytest.mark.parametrize("mode", ["lazy", "eager"])
 @pytest.mark.parametrize("kind", ["urand", "grid", "rmat"])
-def test_lazy_exhaustion_exit(oracle, monkeypatch, kind):
-    """The lazy engine's exhaustion exit (bfs_lazy.cu): on a connected graph the barren last
-    level is accounted without a pull (blest_bfs_last_unpulled = its queue), and levels,
+def test_exhaustion_exit(oracle, monkeypatch, kind, mode):
+    """The engines' exhaustion exit (bfs_lazy.cu, bfs_eager.cu): on a connected graph the
+    barren last level is accounted without a pull (blest_bfs_last_unpulled = its queue), and
+    levels,
     counters and the whole per-level trace still equal the reference engine's, with the exit
     armed (BLEST_EXHAUST=1, default) and off; on RMAT it fires only if the source's component
     holds every vertex with an edge."""
@@ -326,14 +328,16 @@ def test_lazy_exhaustion_exit(oracle, monkeypatch, kind):
     csr = oracle.Csr(g.num_vertices(), off, tgt)
     b = B.build_bvss(g)
     ob = oracle.build_bvss(csr)
+    if mode == "eager":  # the eager count is exact only after a dense level: make them all dense
+        monkeypatch.setenv("BLEST_DENSE_MIN", "1")
     for src in g.pick_sources(3, 11):
         src = int(src)
         want = oracle.reference_bfs(csr, src)[0]
-        o_eng = oracle.run_engine(ob, src, True)
+        o_eng = oracle.run_engine(ob, src, mode == "lazy")
         got = {}
         for ex in ("1", "0"):
             monkeypatch.setenv("BLEST_EXHAUST", ex)
-            res, cnt = run(b, src, "lazy", "popc")
+            res, cnt = run(b, src, mode, "popc")
             unp = C.c_uint64(7)
             L.check(L.lib().blest_bfs_last_unpulled(b.handle, C.byref(unp)))
             assert np.array_equal(res.levels, want), (kind, src, ex)
