@@ -225,8 +225,8 @@ int blest_bfs_levels_device(blest_bvss b, const uint32_t** levels);
 /* Launch geometry of the last run (CTAs, threads per CTA). */
 int blest_bfs_last_geometry(blest_bvss b, uint32_t* ctas, uint32_t* threads);
 /* VSSs of the last finished blest_bfs / blest_bfs_finish run that the counters include but
- * the kernel did not pull: the lazy engine stops pulling once every vertex with an in-edge
- * is visited (the remaining level is provably barren; its trace row is written as the
+ * the kernel did not pull: the engines stop pulling once every vertex with an in-edge
+ * is visited (eager: detected after dense levels) (the remaining level is provably barren; its trace row is written as the
  * reference's would be). Measurement only (bytes actually streamed); no reference counterpart. */
 int blest_bfs_last_unpulled(blest_bvss b, uint64_t* vss);
 
