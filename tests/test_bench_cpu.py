@@ -17,6 +17,19 @@ def test_b_alg_formula():
     assert bench.b_alg(n, D, P, V, L, False) == 648 * D + 4 * P + 4 * n + 4 * V
 
 
+def test_batch_d2h_bytes_follows_the_width_rule():
+    """blest_bfs_batch's narrow transfers (BfsEngine::run_batch): 1 byte per vertex (+ the
+    8-byte deepest level) while levels fit; a source past 254 levels is re-copied as u32 once
+    its copy lands (two sources later) and widens the sources launched after that."""
+    n = 1000
+    assert bench.batch_d2h_bytes([7] * 5, n, packed=False) == 4 * n * 5
+    assert bench.batch_d2h_bytes([7] * 5, n, packed=True) == 5 * (n + 8)
+    # 4 deep sources: 0, 1 go at 1 byte (+ u32 re-copy each); 2, 3 at 2 bytes
+    assert bench.batch_d2h_bytes([300] * 4, n, True) == 2 * (n + 8 + 4 * n) + 2 * (2 * n + 8)
+    # past 65 534 levels: u32 from then on
+    assert bench.batch_d2h_bytes([70000] * 4, n, True) == 2 * (n + 8 + 4 * n) + 2 * 4 * n
+
+
 def test_configs_cover_baseline():
     assert set(bench.CONFIGS) == {"c1", "c2", "c3", "c4", "c5"}
     kind, prm, ordering, _ = bench.CONFIGS["c2"]
