@@ -9,12 +9,17 @@ namespace blestgpu {
 namespace bfsdev {
 
 #ifndef BLEST_KBATCH
-#define BLEST_KBATCH 4
+#define BLEST_KBATCH 2
 #endif
 #ifndef BLEST_KBATCH_LAZY
 #define BLEST_KBATCH_LAZY 3
 #endif
-constexpr int kBatch = BLEST_KBATCH;           // eager: VSSs in flight per warp
+// eager: VSSs per warp batch. The sparse levels of high-diameter graphs are a dependent
+// chain per warp, and a smaller batch spreads a level's VSSs over more warps: 2 vs 4 gives
+// C4 68.3 → 61.0 ms, C1 0.092 → 0.085 ms, C3 with the eager engine 3.97 → 4.11 ms (1: C4
+// 60.8, C3 eager 5.06; 3: 64.2 / 3.75; one build with 3 on dense and 1 on sparse levels
+// spilled and lost both ways: 62.5 / 4.03 — profiles/r02_ekb_ab/)
+constexpr int kBatch = BLEST_KBATCH;
 constexpr int kBatchLazy = BLEST_KBATCH_LAZY;  // lazy (C2: 3 → 1.73 ms, 4 → 1.87, 2 → 2.03)
 constexpr int kPushCap = 64;      // per-warp push buffer entries (eager)
 constexpr unsigned long long kNoEntry = ~0ull;
