@@ -610,6 +610,10 @@ def main():
     balg = np.array([b_alg(n, c["D"] - c["U"], c["P"], c["V"], c["L"] - (1 if c["U"] else 0), lazy)
                      for c in census], np.float64)
     achieved = float(np.sum(balg) / total_s / 1e9)
+    # the same formula on the counters alone (SURVEY 8(d) reads D off the reference's counters,
+    # which include a barren last level the engines account without streaming it)
+    balg_ctr = np.array([b_alg(n, c["D"], c["P"], c["V"], c["L"], lazy) for c in census], np.float64)
+    achieved_ctr = float(np.sum(balg_ctr) / total_s / 1e9)
     peak, peak_kind = load_peaks()
     value, elapsed = hm, total_s
     if world > 1:
@@ -709,7 +713,11 @@ def main():
                           peak_source=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback 6.65 TB/s",
                           algorithmic_bytes_per_bfs=int(np.mean(balg)),
                           formula="648 D + 4 P + 4 n + 4 V + k (n/8) L (SURVEY 8(d)); D and L without a "
-                                  "barren last level the lazy engine did not pull (detail.mean_unpulled)"),
+                                  "barren last level the engine did not pull (detail.mean_unpulled)",
+                          frac_counter_bytes=round(achieved_ctr / peak, 4),
+                          frac_counter_bytes_note="the same formula with D and L straight from the counters "
+                                                  "(the unpulled barren level counted as streamed); equals frac "
+                                                  "when nothing was left unpulled"),
             cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches), parity=parity,
             clocks=clk.summary(),
             detail=dict(grid=[g_ctas.value, g_thr.value], hm_gteps_rank0=round(hm, 4), mean_ms=round(1e3 * float(t.mean()), 4),
